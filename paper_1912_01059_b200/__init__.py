@@ -1,0 +1,27 @@
+"""GGNN (arXiv 1912.01059) graph-based nearest-neighbour search, B200-native.
+
+Drop-in for the reference package `graphann`
+(/root/reference/pkg/src/graphann/__init__.py): same public names and
+signatures; the hot path (query, hierarchical build, sharded search) runs as
+hand-written sm_100a kernels in libggnn_b200.so behind a C ABI
+(include/ggnn_b200.h).  There is no CPU fallback.
+"""
+
+from . import backend
+from .config import BuildConfig, QueryConfig
+from .data import ConfigError, Dataset, FormatError, gen_synthetic, squared_distance
+from .graph import SENTINEL, AdjacencyLayer, GraphStats, Hierarchy
+from .search import (
+    BatchResult,
+    QueryResult,
+    batch_query,
+    greedy_search,
+    hierarchical_query,
+    query,
+    query_arrays,
+    stopping_check,
+    top_layer_seeds,
+)
+from .build import plan_geometry, partition_bottom, select_points
+
+__version__ = "0.1.0"

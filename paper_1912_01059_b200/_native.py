@@ -1,0 +1,159 @@
+"""ctypes binding of libggnn_b200.so (include/ggnn_b200.h).
+
+torch is used only as the device allocator and stream provider: tensors are
+passed to the C ABI as raw device pointers.  There is no fallback -- if the
+library is missing or no CUDA device is present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libggnn_b200.so"
+
+GGNN_F32 = 0
+GGNN_U8 = 1
+FLAG_DISTINCT = 1
+FLAG_EXACT_DISTS = 2
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+F64 = ctypes.c_double
+
+
+class Vectors(ctypes.Structure):
+    _fields_ = [("d_data", P), ("n", I64), ("d", I32), ("dtype", I32)]
+
+
+class Queries(ctypes.Structure):
+    _fields_ = [("d_data", P), ("d_rows", P), ("m", I64), ("dtype", I32), ("pad_", I32)]
+
+
+class Layer(ctypes.Structure):
+    _fields_ = [("d_adj", P), ("d_to_row", P), ("d_down", P), ("node_count", I64), ("k", I32), ("k_nn", I32),
+                ("slack", F64)]
+
+
+class SearchParams(ctypes.Structure):
+    _fields_ = [("k_out", I32), ("prioq_size", I32), ("visited_size", I32), ("flags", I32), ("tau", F64),
+                ("max_iterations", I64)]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+# name -> argtypes (restype is int unless listed in _RESTYPES)
+_SIGS = {
+    "ggnn_last_error": [],
+    "ggnn_version": [],
+    "ggnn_device_info": [P, P],
+    "ggnn_search_workspace_bytes": [I64, P, I32],
+    "ggnn_sanitize_layer": [P, P, I64, I32, I32, P, P],
+    "ggnn_query_batch": [P, P, P, I64, P, P, F64, P, P, P, P, ctypes.c_size_t, P],
+    "ggnn_greedy_batch": [P, P, P, P, P, I32, P, F64, P, P, P, P, ctypes.c_size_t, P],
+    "ggnn_descent_batch": [P, P, I32, I32, I32, P, P, P, P, P, P, P, P, ctypes.c_size_t, P],
+    "ggnn_sym_check_batch": [P, P, P, P, P, I64, F64, F64, I32, I32, I32, I32, I32, P, P, P],
+    "ggnn_exhaustive_topk": [P, P, I64, P, I32, P, P, P],
+    "ggnn_squared_l2_many": [P, P, P, I32, P, P],
+    "ggnn_f32_to_u8": [P, I64, P, P, P],
+    "ggnn_leaf_knn": [P, P, P, P, I64, I64, I32, P, P, P, I32, P, P, P, P],
+}
+_RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t}
+# entry points added by later translation units register themselves here
+EXTRA_SIGS: dict = {}
+
+
+def exported_symbols() -> list[str]:
+    return sorted(list(_SIGS) + list(EXTRA_SIGS))
+
+
+def load(require_gpu: bool = True):
+    """Load the library (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeError(
+            f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, args in {**_SIGS, **EXTRA_SIGS}.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = load().ggnn_last_error()
+        msg = msg.decode() if msg else ""
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+
+
+# ---------------------------------------------------------------- torch glue
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        if not t.cuda.is_available():
+            raise NativeError("no CUDA device visible: the GGNN B200 path has no CPU fallback")
+        _torch = t
+    return _torch
+
+
+def device():
+    return torch().device("cuda", torch().cuda.current_device())
+
+
+def stream_ptr():
+    return P(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> P:
+    return P(0) if t is None else P(t.data_ptr())
+
+
+def to_dev(a: np.ndarray, dtype=None):
+    t = torch()
+    arr = np.ascontiguousarray(a if dtype is None else a.astype(dtype, copy=False))
+    return t.from_numpy(arr).to(device(), non_blocking=False)
+
+
+def empty(shape, dtype):
+    return torch().empty(shape, dtype=dtype, device=device())
+
+
+def vectors_struct(data, dtype_code: int) -> Vectors:
+    n, d = data.shape
+    return Vectors(ptr(data), n, d, dtype_code)
+
+
+def queries_struct(data=None, rows=None, dtype_code: int = GGNN_F32, m: int | None = None) -> Queries:
+    if m is None:
+        m = rows.shape[0] if rows is not None else data.shape[0]
+    return Queries(ptr(data), ptr(rows), m, dtype_code, 0)
+
+
+def search_params(k_out, prioq_size, visited_size, tau, max_iterations, flags=0) -> SearchParams:
+    return SearchParams(int(k_out), int(prioq_size), int(visited_size), int(flags), float(tau), int(max_iterations))

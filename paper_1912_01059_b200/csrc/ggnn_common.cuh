@@ -1,0 +1,370 @@
+// ggnn_common.cuh -- shared device building blocks for the GGNN sm_100a kernels.
+//
+// Layout conventions:
+//   vectors  : row-major (n, d), either float32 or uint8 (lossless copy of
+//              integer-valued data in [0, 255]); rows are 16-byte aligned when
+//              d * elem_size is a multiple of 16.
+//   adjacency: row-major int32 (node_count, k), "sanitized": every slot the
+//              reference would skip is -1 (direct slots holding -1, sym slots at
+//              or beyond sym_count), so the kernels need no sym_count array.
+//   keys     : distances are carried as exact uint32 for uint8 data (the sum of
+//              squared byte differences) and as double for float data, matching
+//              the reference's float64 accumulation (_core.pyx:30-37).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+namespace ggnn {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WARP = 32;
+constexpr int MAX_K = 32;  // slots per adjacency row handled by one warp
+
+enum Term : int { TERM_STOP = 0, TERM_EMPTY = 1, TERM_CAP = 2 };
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- key types
+template <typename K> struct KeyOps;
+template <> struct KeyOps<uint32_t> {
+  static __device__ __forceinline__ uint32_t max_key() { return 0xffffffffu; }
+  static __device__ __forceinline__ double to_d(uint32_t k) { return (double)k; }
+  static __device__ __forceinline__ uint32_t from_d(double v) { return (uint32_t)v; }
+  static __device__ __forceinline__ uint32_t shfl(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
+  static __device__ __forceinline__ uint32_t shfl_xor(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
+};
+template <> struct KeyOps<double> {
+  static __device__ __forceinline__ double max_key() { return __longlong_as_double(0x7ff0000000000000ll); }
+  static __device__ __forceinline__ double to_d(double k) { return k; }
+  static __device__ __forceinline__ double from_d(double v) { return v; }
+  static __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(FULL, v, src); }
+  static __device__ __forceinline__ double shfl_xor(double v, int m) { return __shfl_xor_sync(FULL, v, m); }
+};
+
+template <typename K>
+__device__ __forceinline__ bool key_less(K ka, int ia, K kb, int ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+// Bitonic sort of one (key, id) pair per lane, ascending by (key, id).
+template <typename K>
+__device__ __forceinline__ void warp_sort(K& key, int& id) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      K ok = KeyOps<K>::shfl_xor(key, stride);
+      int oi = __shfl_xor_sync(FULL, id, stride);
+      bool up = ((lane & size) == 0);       // ascending block
+      bool lower = ((lane & stride) == 0);  // I hold the lower index of the pair
+      bool other_less = key_less(ok, oi, key, id);
+      // lower lane keeps the min in an ascending block, the max otherwise
+      bool take = (lower == up) ? other_less : !other_less && !(ok == key && oi == id);
+      if (take) {
+        key = ok;
+        id = oi;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- vectors
+// Query storage: float queries are kept as float in shared memory, uint8
+// queries as uint8.  Distances:
+//   float data / float query : double accumulation of ((double)x - (double)q)^2
+//   uint8 data / uint8 query : exact uint32 sum of squared byte differences
+//   uint8 data / float query : double accumulation (non-integral queries)
+template <typename TX, typename TQ> struct VecTraits;
+template <> struct VecTraits<float, float> { using Key = double; };
+template <> struct VecTraits<uint8_t, uint8_t> { using Key = uint32_t; };
+template <> struct VecTraits<uint8_t, float> { using Key = double; };
+
+// Partial distance of the elements [e0, e0+CH) handled by one lane.
+__device__ __forceinline__ double part_f32(const float4 a, const float* q) {
+  double d0 = (double)a.x - (double)q[0], d1 = (double)a.y - (double)q[1];
+  double d2 = (double)a.z - (double)q[2], d3 = (double)a.w - (double)q[3];
+  double s = d0 * d0;
+  s = fma(d1, d1, s);
+  s = fma(d2, d2, s);
+  return fma(d3, d3, s);
+}
+__device__ __forceinline__ uint32_t sad_sq4(uint32_t a, uint32_t b, uint32_t acc) {
+  uint32_t ad = __vabsdiffu4(a, b);
+  return __dp4a(ad, ad, acc);
+}
+__device__ __forceinline__ uint32_t part_u8(const uint4 a, const uint4 q) {
+  uint32_t s = sad_sq4(a.x, q.x, 0u);
+  s = sad_sq4(a.y, q.y, s);
+  s = sad_sq4(a.z, q.z, s);
+  return sad_sq4(a.w, q.w, s);
+}
+
+// Distances of `cnt` compacted candidate rows (rows[c], c < cnt, in shared
+// memory) to the query qs (shared memory); results go to kout[c] (shared).
+// Rows are read with 16-byte vector loads; LPR lanes cooperate on one row
+// (LPR = power of two >= 16-byte chunks per row, at most 32), so one load
+// instruction covers 32/LPR rows, and UNR row groups are issued before any
+// is consumed so their latencies overlap.  Callers __syncwarp() afterwards.
+template <int LPR, typename Acc>
+__device__ __forceinline__ Acc group_reduce(Acc v) {
+#pragma unroll
+  for (int o = LPR >> 1; o > 0; o >>= 1) v += KeyOps<Acc>::shfl_xor(v, o);
+  return v;
+}
+
+template <int LPR, int UNR>
+__device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const float* qs, const int* rows, int cnt,
+                                              double* kout) {
+  const int lane = lane_id();
+  const int nch = (int)(d >> 2);
+  constexpr int RPP = 32 / LPR;
+  const int sub = lane & (LPR - 1);
+  const int grp = lane / LPR;
+  for (int base = 0; base < cnt; base += RPP * UNR) {
+    double acc[UNR];
+    const float4* rp[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      int ci = base + u * RPP + grp;
+      int r = ci < cnt ? rows[ci] : -1;
+      rp[u] = r >= 0 ? reinterpret_cast<const float4*>(X + (int64_t)r * d) : nullptr;
+      acc[u] = 0.0;
+    }
+    for (int c = sub; c < nch; c += LPR) {
+      float4 v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (rp[u]) v[u] = __ldg(rp[u] + c);
+      const float* qc = qs + 4 * c;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (rp[u]) acc[u] += part_f32(v[u], qc);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      double t = group_reduce<LPR, double>(acc[u]);
+      int ci = base + u * RPP + grp;
+      if (sub == 0 && ci < cnt) kout[ci] = t;
+    }
+  }
+}
+
+template <int LPR, int UNR>
+__device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const uint8_t* qs, const int* rows,
+                                             int cnt, uint32_t* kout) {
+  const int lane = lane_id();
+  const int nch = (int)(d >> 4);
+  constexpr int RPP = 32 / LPR;
+  const int sub = lane & (LPR - 1);
+  const int grp = lane / LPR;
+  for (int base = 0; base < cnt; base += RPP * UNR) {
+    uint32_t acc[UNR];
+    const uint4* rp[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      int ci = base + u * RPP + grp;
+      int r = ci < cnt ? rows[ci] : -1;
+      rp[u] = r >= 0 ? reinterpret_cast<const uint4*>(X + (int64_t)r * d) : nullptr;
+      acc[u] = 0u;
+    }
+    for (int c = sub; c < nch; c += LPR) {
+      uint4 v[UNR];
+      const uint4 qv = reinterpret_cast<const uint4*>(qs)[c];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (rp[u]) v[u] = __ldg(rp[u] + c);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (rp[u]) acc[u] += part_u8(v[u], qv);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      uint32_t t = group_reduce<LPR, uint32_t>(acc[u]);
+      int ci = base + u * RPP + grp;
+      if (sub == 0 && ci < cnt) kout[ci] = t;
+    }
+  }
+}
+
+// scalar fallbacks (any d, any alignment): one row at a time, lanes stride d
+template <typename TX, typename TQ, typename Key>
+__device__ __forceinline__ void dists_scalar(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
+                                             Key* kout) {
+  const int lane = lane_id();
+  for (int c = 0; c < cnt; ++c) {
+    const TX* xr = X + (int64_t)rows[c] * d;
+    Key s = 0;
+    for (int64_t e = lane; e < d; e += 32) {
+      if constexpr (sizeof(Key) == 4) {
+        int df = (int)xr[e] - (int)qs[e];
+        s += (Key)(df * df);
+      } else {
+        double df = (double)xr[e] - (double)qs[e];
+        s = fma(df, df, s);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += KeyOps<Key>::shfl_xor(s, o);
+    if (lane == 0) kout[c] = s;
+  }
+}
+
+template <typename TX, typename TQ>
+__device__ __forceinline__ void warp_dists(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
+                                           typename VecTraits<TX, TQ>::Key* kout, int lpr) {
+  if constexpr (std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {
+    switch (lpr) {
+      case 32: dists_f32_vec<32, 8>(X, d, qs, rows, cnt, kout); return;
+      case 16: dists_f32_vec<16, 4>(X, d, qs, rows, cnt, kout); return;
+      case 8: dists_f32_vec<8, 4>(X, d, qs, rows, cnt, kout); return;
+      case 4: dists_f32_vec<4, 2>(X, d, qs, rows, cnt, kout); return;
+      case 2: dists_f32_vec<2, 2>(X, d, qs, rows, cnt, kout); return;
+      case 1: dists_f32_vec<1, 1>(X, d, qs, rows, cnt, kout); return;
+      default: break;
+    }
+  } else if constexpr (std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
+    switch (lpr) {
+      case 32: dists_u8_vec<32, 4>(X, d, qs, rows, cnt, kout); return;
+      case 16: dists_u8_vec<16, 4>(X, d, qs, rows, cnt, kout); return;
+      case 8: dists_u8_vec<8, 8>(X, d, qs, rows, cnt, kout); return;
+      case 4: dists_u8_vec<4, 4>(X, d, qs, rows, cnt, kout); return;
+      case 2: dists_u8_vec<2, 2>(X, d, qs, rows, cnt, kout); return;
+      case 1: dists_u8_vec<1, 1>(X, d, qs, rows, cnt, kout); return;
+      default: break;
+    }
+  }
+  dists_scalar<TX, TQ>(X, d, qs, rows, cnt, kout);
+}
+
+// Lanes-per-row code for the vectorised paths (0 = scalar fallback).
+inline int choose_lpr(int64_t d, int dtype_x, int dtype_q, uintptr_t base) {
+  int chunk = 0;
+  if (dtype_x == 0 && dtype_q == 0) chunk = 4;
+  if (dtype_x == 1 && dtype_q == 1) chunk = 16;
+  if (!chunk || d % chunk != 0 || (base & 15)) return 0;
+  int64_t nch = d / chunk;
+  int lpr = 1;
+  while (lpr < nch && lpr < 32) lpr <<= 1;
+  return lpr;
+}
+
+// Exact sequential float64 squared distance, the reference's _sqdist
+// (_core.pyx:30-37) operation for operation: no FMA contraction.
+template <typename TX, typename TQ>
+__device__ __forceinline__ double seq_sqdist(const TX* xr, const TQ* q, int64_t d) {
+  double acc = 0.0;
+  for (int64_t i = 0; i < d; ++i) {
+    double df = __dsub_rn((double)xr[i], (double)q[i]);
+    acc = __dadd_rn(acc, __dmul_rn(df, df));
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------- membership
+// Open-addressing refcount table in shared memory (one per warp).
+//   slot == 0          : empty
+//   slot == 0xffffffff : tombstone
+//   otherwise          : (count << 30) | node, count in 1..3, node < 2^30 - 1
+struct RefTable {
+  uint32_t* t;
+  uint32_t mask;
+  int shift;
+  static constexpr uint32_t EMPTY = 0u, TOMB = 0xffffffffu, KMASK = (1u << 30) - 1u, ONE = 1u << 30;
+
+  __device__ __forceinline__ uint32_t home(uint32_t key) const { return (key * 2654435761u) >> shift; }
+
+  // per-lane lookup: count of `key` (0 if absent)
+  __device__ __forceinline__ uint32_t count(uint32_t key) const {
+    uint32_t s = home(key);
+    for (;;) {
+      uint32_t v = t[s];
+      if (v == EMPTY) return 0u;
+      if (v != TOMB && (v & KMASK) == key) return v >> 30;
+      s = (s + 1) & mask;
+    }
+  }
+  // per-lane insert of an absent key with count 1; returns 1 if an empty slot was consumed
+  __device__ __forceinline__ int insert_new(uint32_t key) {
+    uint32_t s = home(key);
+    for (;;) {
+      uint32_t v = t[s];
+      if (v == EMPTY || v == TOMB) {
+        uint32_t old = atomicCAS(&t[s], v, ONE | key);
+        if (old == v) return v == EMPTY ? 1 : 0;
+        continue;  // lost the race, re-read this slot
+      }
+      s = (s + 1) & mask;
+    }
+  }
+  // per-lane insert-or-increment (used by rebuild; no tombstones present)
+  __device__ __forceinline__ int add_one(uint32_t key) {
+    uint32_t s = home(key);
+    for (;;) {
+      uint32_t v = t[s];
+      if (v == EMPTY) {
+        uint32_t old = atomicCAS(&t[s], EMPTY, ONE | key);
+        if (old == EMPTY) return 1;
+        continue;
+      }
+      if ((v & KMASK) == key) {
+        atomicAdd(&t[s], ONE);
+        return 0;
+      }
+      s = (s + 1) & mask;
+    }
+  }
+  // warp-cooperative location of a live key (uniform result, -1 if absent)
+  __device__ __forceinline__ int find_slot(uint32_t key) const {
+    const int lane = lane_id();
+    uint32_t s0 = home(key);
+    for (uint32_t off = 0;; off += 32) {
+      uint32_t s = (s0 + off + lane) & mask;
+      uint32_t v = t[s];
+      unsigned hit = __ballot_sync(FULL, v != TOMB && v != EMPTY && (v & KMASK) == key);
+      unsigned emp = __ballot_sync(FULL, v == EMPTY);
+      if (hit && (!emp || __ffs(hit) < __ffs(emp))) return (int)((s0 + off + __ffs(hit) - 1) & mask);
+      if (emp) return -1;
+    }
+  }
+  // decrement (warp-uniform call); returns true when the count reached zero
+  __device__ __forceinline__ bool dec(uint32_t key) {
+    int s = find_slot(key);
+    bool zero = false;
+    if (s >= 0) {
+      uint32_t v = t[s];
+      zero = (v >> 30) == 1u;
+      __syncwarp();
+      if (lane_id() == 0) t[s] = zero ? TOMB : v - ONE;
+    }
+    __syncwarp();
+    return zero;
+  }
+  __device__ __forceinline__ void inc(uint32_t key) {
+    int s = find_slot(key);
+    if (s >= 0) {
+      uint32_t v = t[s];
+      __syncwarp();
+      if (lane_id() == 0) t[s] = v + ONE;
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void tomb(uint32_t key) {
+    int s = find_slot(key);
+    __syncwarp();
+    if (s >= 0 && lane_id() == 0) t[s] = TOMB;
+    __syncwarp();
+  }
+  __device__ __forceinline__ void clear() {
+    for (uint32_t i = lane_id(); i <= mask; i += 32) t[i] = EMPTY;
+    __syncwarp();
+  }
+};
+
+}  // namespace ggnn

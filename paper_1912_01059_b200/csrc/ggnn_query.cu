@@ -1,0 +1,737 @@
+// ggnn_query.cu -- search kernels (query, greedy, descent, sym-check, top-k)
+// and their C-ABI entry points (include/ggnn_b200.h).
+//
+// Launch shape: one warp per search, W warps per CTA, each warp owning a
+// private shared-memory region (ring + visited ring + refcount table + query).
+// Every search is independent, so the grid is simply ceil(m / W) CTAs and the
+// hardware block scheduler balances the (very uneven) per-query work.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "ggnn_capi_util.cuh"
+#include "ggnn_search.cuh"
+
+namespace ggnn {
+
+static thread_local std::string g_err;
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+DevInfo dev_info() {
+  static DevInfo info{0, 0};
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&info.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&info.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  });
+  return info;
+}
+
+constexpr int MAX_LAYERS = 24;
+
+struct LayerDev {
+  const int32_t* adj;
+  const int32_t* to_row;
+  const int32_t* down;
+  int64_t node_count;
+  int k;
+  double slack;
+};
+
+struct SearchArgs {
+  const void* X;
+  int64_t n;
+  int64_t d;
+  int lpr;
+  const void* Q;        // query table (TQ) or nullptr
+  const int32_t* qrows; // rows of X used as queries, or nullptr
+  int64_t m;
+  SearchCfg c;
+  size_t region;        // bytes per warp
+  int32_t* ids;
+  double* dists;
+  int32_t* counters;
+  uint32_t* ever;       // m * ever_size entries, or nullptr
+  uint32_t ever_size;
+  // query()
+  const int32_t* top_rows;
+  int64_t ntop;
+  double dmax;
+  LayerDev layer;
+  // greedy
+  const int32_t* seed_ids;
+  const double* seed_dists;
+  int nseeds;
+  // descent
+  LayerDev layers[MAX_LAYERS];
+  int start, stop;
+  const int32_t* seg_lo;
+  const int32_t* seg_hi;
+};
+
+template <typename TX, typename TQ>
+__device__ __forceinline__ void load_query(TQ* qs, const SearchArgs& a, int64_t qi) {
+  const int lane = lane_id();
+  const TQ* src;
+  if (a.qrows) {
+    src = reinterpret_cast<const TQ*>(a.X) + (int64_t)__ldg(a.qrows + qi) * a.d;
+  } else {
+    src = reinterpret_cast<const TQ*>(a.Q) + qi * a.d;
+  }
+  for (int64_t e = lane; e < a.d; e += 32) qs[e] = src[e];
+  __syncwarp();
+}
+
+template <typename TX, typename TQ>
+__device__ __forceinline__ void init_search(WarpSearch<TX, TQ>& s, const SearchArgs& a, uint8_t* region, int64_t qi) {
+  s.X = reinterpret_cast<const TX*>(a.X);
+  s.d = a.d;
+  s.lpr = a.lpr;
+  s.c = a.c;
+  s.target = -1;
+  s.carve(region);
+  s.ever = a.ever ? a.ever + (size_t)qi * a.ever_size : nullptr;
+  s.ever_mask = a.ever_size - 1u;
+}
+
+template <typename TX, typename TQ>
+__device__ __forceinline__ void zero_ever(WarpSearch<TX, TQ>& s, uint32_t size) {
+  if (!s.ever) return;
+  for (uint32_t i = lane_id(); i < size; i += 32) s.ever[i] = 0u;
+  __syncwarp();
+  __threadfence_block();
+}
+
+template <typename TX, typename TQ>
+__device__ __forceinline__ void set_layer(WarpSearch<TX, TQ>& s, const LayerDev& L) {
+  s.adj = L.adj;
+  s.k = L.k;
+  s.to_row = L.to_row;
+  s.dmax = L.slack;
+}
+
+// hits -> output rows; float keys optionally re-scored sequentially
+template <typename TX, typename TQ>
+__device__ void write_hits(const WarpSearch<TX, TQ>& s, const SearchArgs& a, int64_t qi, const int32_t* to_row,
+                           int extra_visited, int extra_distinct) {
+  using Key = typename VecTraits<TX, TQ>::Key;
+  const int lane = lane_id();
+  Key key;
+  int id;
+  const int nh = s.hits(key, id);
+  const int k_out = a.c.k_out;
+  if (lane < k_out) {
+    double dv = __longlong_as_double(0x7ff0000000000000ll);
+    if (lane < nh) {
+      dv = KeyOps<Key>::to_d(key);
+      if constexpr (sizeof(Key) == 8) {
+        if (a.c.flags & FLAG_EXACT_DISTS) {
+          int row = to_row ? __ldg(to_row + id) : id;
+          dv = seq_sqdist<TX, TQ>(s.X + (int64_t)row * a.d, s.qs, a.d);
+        }
+      }
+    }
+    a.ids[qi * k_out + lane] = lane < nh ? id : -1;
+    a.dists[qi * k_out + lane] = dv;
+  }
+  if (lane == 0 && a.counters) {
+    int32_t* c = a.counters + qi * 5;
+    c[0] = s.visited + extra_visited;
+    c[1] = s.steps;
+    c[2] = s.term;
+    c[3] = s.distinct + extra_distinct;
+    c[4] = s.forgotten;
+  }
+}
+
+// ------------------------------------------------------------------ query()
+template <typename TX, typename TQ>
+__global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using Key = typename VecTraits<TX, TQ>::Key;
+  const int wib = threadIdx.x >> 5;
+  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (qi >= a.m) return;
+  const int lane = lane_id();
+  WarpSearch<TX, TQ> s;
+  init_search(s, a, smem + (size_t)wib * a.region, qi);
+  load_query<TX, TQ>(s.qs, a, qi);
+  set_layer(s, a.layer);
+  s.dmax = a.dmax;
+  s.reset();
+  zero_ever(s, a.ever_size);
+  // top_layer_seeds (search.py:100-112): exact top-min(k_out, ntop) over the top layer
+  const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
+  Key bk;
+  int bi;
+  warp_topk_scan<TX, TQ>(s.X, a.d, s.qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, s.crow, s.ckey, bk, bi);
+  int sid = -1;
+  if (lane < kk) sid = a.top_rows ? __ldg(a.top_rows + bi) : bi;
+  s.seed(bk, sid, kk);
+  s.run();
+  // query() adds the top scan to the effort counters (search.py:134-136)
+  write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
+}
+
+// ------------------------------------------------------------ greedy_search
+template <typename TX, typename TQ>
+__global__ void __launch_bounds__(256) greedy_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using Key = typename VecTraits<TX, TQ>::Key;
+  const int wib = threadIdx.x >> 5;
+  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (qi >= a.m) return;
+  const int lane = lane_id();
+  WarpSearch<TX, TQ> s;
+  init_search(s, a, smem + (size_t)wib * a.region, qi);
+  load_query<TX, TQ>(s.qs, a, qi);
+  set_layer(s, a.layer);
+  s.dmax = a.dmax;
+  s.reset();
+  zero_ever(s, a.ever_size);
+  for (int base = 0; base < a.nseeds; base += 32) {
+    const int cnt = min(32, a.nseeds - base);
+    int sid = -1;
+    Key sk = KeyOps<Key>::max_key();
+    if (lane < cnt) {
+      sid = a.seed_ids[qi * a.nseeds + base + lane];
+      sk = KeyOps<Key>::from_d(a.seed_dists[qi * a.nseeds + base + lane]);
+    }
+    s.seed(sk, sid, cnt);
+  }
+  s.run();
+  write_hits(s, a, qi, a.layer.to_row, 0, 0);
+}
+
+// ------------------------------------------------------- hierarchical_query
+template <typename TX, typename TQ>
+__global__ void __launch_bounds__(256) descent_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using Key = typename VecTraits<TX, TQ>::Key;
+  const int wib = threadIdx.x >> 5;
+  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (qi >= a.m) return;
+  const int lane = lane_id();
+  WarpSearch<TX, TQ> s;
+  init_search(s, a, smem + (size_t)wib * a.region, qi);
+  load_query<TX, TQ>(s.qs, a, qi);
+  const LayerDev& Ls = a.layers[a.start];
+  const int lo = a.seg_lo ? __ldg(a.seg_lo + qi) : 0;
+  const int hi = a.seg_hi ? __ldg(a.seg_hi + qi) : (int)Ls.node_count;
+  const int kk = min(a.c.k_out, hi - lo);
+  Key bk;
+  int bi;
+  warp_topk_scan<TX, TQ>(s.X, a.d, s.qs, a.lpr, Ls.to_row, lo, hi, kk, s.crow, s.ckey, bk, bi);
+  int id = lane < kk ? bi + lo : -1;
+  int nh = kk;
+  int visited = hi - lo, steps = 0, distinct = (hi - lo) - kk, forgotten = 0, term = TERM_EMPTY;
+  for (int j = a.start - 1; j >= a.stop; --j) {
+    const LayerDev& Lj = a.layers[j];
+    const int sid = lane < nh ? __ldg(a.layers[j + 1].down + id) : -1;
+    set_layer(s, Lj);
+    s.reset();
+    zero_ever(s, a.ever_size);
+    s.seed(bk, sid, nh);
+    s.run();
+    visited += s.visited;
+    steps += s.steps;
+    distinct += s.distinct;
+    forgotten += s.forgotten;
+    term = s.term;
+    nh = s.hits(bk, id);
+  }
+  const int k_out = a.c.k_out;
+  const int32_t* stop_rows = a.layers[a.stop].to_row;
+  if (lane < k_out) {
+    double dv = __longlong_as_double(0x7ff0000000000000ll);
+    if (lane < nh) {
+      dv = KeyOps<Key>::to_d(bk);
+      if constexpr (sizeof(Key) == 8) {
+        if (a.c.flags & FLAG_EXACT_DISTS) {
+          int row = stop_rows ? __ldg(stop_rows + id) : id;
+          dv = seq_sqdist<TX, TQ>(s.X + (int64_t)row * a.d, s.qs, a.d);
+        }
+      }
+    }
+    a.ids[qi * k_out + lane] = lane < nh ? id : -1;
+    a.dists[qi * k_out + lane] = dv;
+  }
+  if (lane == 0 && a.counters) {
+    int32_t* c = a.counters + qi * 5;
+    c[0] = visited;
+    c[1] = steps;
+    c[2] = term;
+    c[3] = distinct;
+    c[4] = forgotten;
+  }
+}
+
+// ----------------------------------------------------------- sym_check_pair
+struct SymArgs {
+  const void* X;
+  int64_t d;
+  int lpr;
+  LayerDev layer;
+  const int32_t* px;
+  const int32_t* pz;
+  const double* pd;
+  int64_t npairs;
+  SearchCfg c;
+  double dmax;
+  size_t region;
+  int n_fallback;
+  int32_t* verdict;
+  int32_t* fallback;
+};
+
+template <typename TX>
+__global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ SymArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using Key = typename VecTraits<TX, TX>::Key;
+  const int wib = threadIdx.x >> 5;
+  const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (pi >= a.npairs) return;
+  const int lane = lane_id();
+  const int x = __ldg(a.px + pi), z = __ldg(a.pz + pi);
+  // verdict 0: x already sits in one of z's slots (_core.pyx:405-408)
+  int slot = lane < a.layer.k ? __ldg(a.layer.adj + (int64_t)z * a.layer.k + lane) : -1;
+  const bool present = __any_sync(FULL, slot == x);
+  int32_t* fb = a.fallback + pi * a.n_fallback;
+  if (present) {
+    if (lane == 0) a.verdict[pi] = 0;
+    for (int j = lane; j < a.n_fallback; j += 32) fb[j] = -1;
+    return;
+  }
+  WarpSearch<TX, TX> s;
+  s.X = reinterpret_cast<const TX*>(a.X);
+  s.d = a.d;
+  s.lpr = a.lpr;
+  s.c = a.c;
+  s.target = x;
+  s.carve(smem + (size_t)wib * a.region);
+  s.ever = nullptr;
+  s.ever_mask = 0;
+  set_layer(s, a.layer);
+  s.dmax = a.dmax;
+  const int xrow = a.layer.to_row ? __ldg(a.layer.to_row + x) : x;
+  const TX* src = s.X + (int64_t)xrow * a.d;
+  for (int64_t e = lane; e < a.d; e += 32) s.qs[e] = src[e];
+  __syncwarp();
+  s.reset();
+  s.seed(KeyOps<Key>::from_d(a.pd[pi]), lane == 0 ? z : -1, 1);
+  s.run();
+  const int v = s.term ? 1 : 2;
+  if (lane == 0) a.verdict[pi] = v;
+  // fallbacks: closest explored ids excluding x and z (_core.pyx:420-426)
+  int cand = -1;
+  const int nh = min(s.L, a.c.k_out);
+  if (v == 2 && lane < nh) cand = s.rid[lane];
+  const bool keep = cand >= 0 && cand != x && cand != z;
+  const unsigned km = __ballot_sync(FULL, keep);
+  const int rank = __popc(km & lanemask_lt());
+  if (keep && rank < a.n_fallback) fb[rank] = cand;
+  const int w = min(__popc(km), a.n_fallback);
+  for (int j = w + lane; j < a.n_fallback; j += 32) fb[j] = -1;
+}
+
+// ----------------------------------------------------------- exhaustive_topk
+template <typename TX, typename TQ>
+__global__ void __launch_bounds__(256) topk_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using Key = typename VecTraits<TX, TQ>::Key;
+  const int wib = threadIdx.x >> 5;
+  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (qi >= a.m) return;
+  const int lane = lane_id();
+  uint8_t* base = smem + (size_t)wib * a.region;
+  int* crow = reinterpret_cast<int*>(base);
+  Key* ckey = reinterpret_cast<Key*>(base + 128);
+  TQ* qs = reinterpret_cast<TQ*>(base + 128 + align16(32 * sizeof(Key)));
+  load_query<TX, TQ>(qs, a, qi);
+  const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
+  Key bk;
+  int bi;
+  warp_topk_scan<TX, TQ>(reinterpret_cast<const TX*>(a.X), a.d, qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, crow,
+                         ckey, bk, bi);
+  const int k_out = a.c.k_out;
+  if (lane < k_out) {
+    double dv = __longlong_as_double(0x7ff0000000000000ll);
+    if (lane < kk) {
+      dv = KeyOps<Key>::to_d(bk);
+      if constexpr (sizeof(Key) == 8) {
+        int row = a.top_rows ? __ldg(a.top_rows + bi) : bi;
+        dv = seq_sqdist<TX, TQ>(reinterpret_cast<const TX*>(a.X) + (int64_t)row * a.d, qs, a.d);
+      }
+    }
+    a.ids[qi * k_out + lane] = lane < kk ? bi : -1;
+    a.dists[qi * k_out + lane] = dv;
+  }
+}
+
+// --------------------------------------------------------- squared_l2_many
+template <typename TX, typename TQ>
+__global__ void sqdist_kernel(const TX* X, int64_t d, const TQ* Q, const int32_t* qrows, const int32_t* rows,
+                              int per_query, int64_t total, double* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int64_t qi = i / per_query;
+  const TQ* q = qrows ? reinterpret_cast<const TQ*>(X) + (int64_t)qrows[qi] * d : Q + qi * d;
+  out[i] = seq_sqdist<TX, TQ>(X + (int64_t)rows[i] * d, q, d);
+}
+
+// ----------------------------------------------------------------- helpers
+__global__ void sanitize_kernel(const int32_t* adj, const int32_t* symc, int64_t n, int k, int k_nn, int32_t* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * k) return;
+  int64_t node = i / k;
+  int j = (int)(i - node * k);
+  int32_t v = adj[i];
+  bool keep = j < k_nn ? v >= 0 : (j < k_nn + (symc ? symc[node] : 0));
+  out[i] = keep ? v : -1;
+}
+
+__global__ void f32_to_u8_kernel(const float* src, int64_t count, uint8_t* dst, int32_t* flag) {
+  int ok = 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = src[i];
+    bool good = v >= 0.0f && v <= 255.0f && v == rintf(v);
+    ok &= good ? 1 : 0;
+    if (dst) dst[i] = good ? (uint8_t)v : 0;
+  }
+  if (!__all_sync(FULL, ok) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
+}
+
+}  // namespace ggnn
+
+using namespace ggnn;
+
+// ========================================================================= C ABI
+namespace {
+
+LayerDev to_dev(const ggnn_layer& l) {
+  LayerDev d;
+  d.adj = l.d_adj;
+  d.to_row = l.d_to_row;
+  d.down = l.d_down;
+  d.node_count = l.node_count;
+  d.k = l.k;
+  d.slack = l.slack;
+  return d;
+}
+
+int validate_params(const ggnn_search_params* p) {
+  GGNN_CHECK_ARG(p != nullptr, "null search params");
+  GGNN_CHECK_ARG(p->k_out >= 1 && p->k_out <= 32, "k_out must be in [1, 32] on the GPU path (got %d)", p->k_out);
+  GGNN_CHECK_ARG(p->prioq_size >= 1 && p->visited_size >= 1, "cache geometry values must be >= 1");
+  GGNN_CHECK_ARG(p->max_iterations >= 0, "max_iterations must be >= 0");
+  return GGNN_OK;
+}
+
+SearchCfg make_cfg(const ggnn_search_params* p) {
+  SearchCfg c;
+  c.k_out = p->k_out;
+  c.cap = p->k_out + p->prioq_size;
+  c.vsz = p->visited_size;
+  c.hlog = table_log2(c.cap, c.vsz);
+  c.tau = p->tau;
+  c.max_steps = p->max_iterations;
+  c.flags = p->flags;
+  return c;
+}
+
+// choose warps per CTA so that the CTA fits in shared memory
+int pick_warps(size_t region, int want) {
+  DevInfo di = dev_info();
+  size_t limit = di.smem_optin > 0 ? (size_t)di.smem_optin : (size_t)48 * 1024;
+  int w = want;
+  while (w > 1 && (size_t)w * region > limit) --w;
+  return ((size_t)w * region > limit) ? 0 : w;
+}
+
+template <typename Kern>
+int launch_warps(Kern kern, const SearchArgs& a, int64_t items, size_t region, cudaStream_t st, int want = 4) {
+  if (items <= 0) return GGNN_OK;
+  int W = pick_warps(region, want);
+  GGNN_CHECK_ARG(W > 0, "search state of %zu bytes does not fit in shared memory", region);
+  size_t smem = (size_t)W * region;
+  GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t grid = (items + W - 1) / W;
+  kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int qelem_of(int dtype) { return dtype == GGNN_U8 ? 1 : 4; }
+
+int fill_common(SearchArgs& a, const ggnn_vectors* X, const ggnn_queries* Q, const ggnn_search_params* p) {
+  GGNN_CHECK_ARG(X && X->d_data && X->d > 0 && X->n > 0, "invalid vector table");
+  GGNN_CHECK_ARG(X->dtype == GGNN_F32 || X->dtype == GGNN_U8, "unknown vector dtype %d", X->dtype);
+  GGNN_CHECK_ARG(Q && (Q->d_data || Q->d_rows) && Q->m >= 0, "invalid queries");
+  int qd = Q->d_rows ? X->dtype : Q->dtype;
+  GGNN_CHECK_ARG(qd == GGNN_F32 || qd == GGNN_U8, "unknown query dtype %d", qd);
+  GGNN_CHECK_ARG(!(X->dtype == GGNN_F32 && qd == GGNN_U8), "uint8 queries need uint8 vectors");
+  int rc = validate_params(p);
+  if (rc) return rc;
+  memset(&a, 0, sizeof(a));
+  a.X = X->d_data;
+  a.n = X->n;
+  a.d = X->d;
+  a.lpr = choose_lpr(X->d, X->dtype, qd, reinterpret_cast<uintptr_t>(X->d_data));
+  a.Q = Q->d_rows ? nullptr : Q->d_data;
+  a.qrows = Q->d_rows;
+  a.m = Q->m;
+  a.c = make_cfg(p);
+  int keysize = (X->dtype == GGNN_U8 && qd == GGNN_U8) ? 4 : 8;
+  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(qd), keysize);
+  return GGNN_OK;
+}
+
+int combo(const ggnn_vectors* X, const ggnn_queries* Q) {
+  int qd = Q->d_rows ? X->dtype : Q->dtype;
+  if (X->dtype == GGNN_F32) return 0;          // f32 / f32
+  return qd == GGNN_U8 ? 1 : 2;                // u8 / u8, u8 / f32
+}
+
+uint32_t ever_size_for(const ggnn_search_params* p, int32_t max_seeds, int k) {
+  uint64_t need = 2ull * ((uint64_t)max_seeds + (uint64_t)std::max<int64_t>(p->max_iterations, 1) * (uint64_t)k) + 64;
+  uint32_t e = 64;
+  while (e < need && e < (1u << 30)) e <<= 1;
+  return e;
+}
+
+int attach_ever(SearchArgs& a, const ggnn_search_params* p, int32_t max_seeds, int k, void* ws, size_t wsb) {
+  if (!(p->flags & GGNN_FLAG_DISTINCT)) return GGNN_OK;
+  uint32_t e = ever_size_for(p, max_seeds, k);
+  size_t need = (size_t)a.m * e * 4;
+  GGNN_CHECK_ARG(ws != nullptr && wsb >= need, "GGNN_FLAG_DISTINCT needs %zu bytes of workspace", need);
+  a.ever = reinterpret_cast<uint32_t*>(ws);
+  a.ever_size = e;
+  return GGNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ggnn_last_error(void) { return g_err.c_str(); }
+int ggnn_version(void) { return 100; }
+
+int ggnn_device_info(int* sm_count, int* smem_per_block) {
+  DevInfo di = dev_info();
+  if (sm_count) *sm_count = di.sm_count;
+  if (smem_per_block) *smem_per_block = di.smem_optin;
+  return di.sm_count > 0 ? GGNN_OK : GGNN_E_CUDA;
+}
+
+size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params* p, int32_t max_seeds) {
+  if (!p || !(p->flags & GGNN_FLAG_DISTINCT)) return 0;
+  return (size_t)m * ever_size_for(p, max_seeds, MAX_K) * 4;
+}
+
+int ggnn_sanitize_layer(const int32_t* d_adj, const int32_t* d_sym_count, int64_t node_count, int32_t k,
+                        int32_t k_nn, int32_t* d_out, void* stream) {
+  GGNN_CHECK_ARG(d_adj && d_out && node_count >= 0 && k >= 1 && k <= MAX_K && k_nn >= 1 && k_nn <= k,
+                 "invalid layer geometry (k=%d, k_nn=%d; k <= %d supported)", k, k_nn, MAX_K);
+  int64_t total = node_count * k;
+  if (total == 0) return GGNN_OK;
+  sanitize_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(d_adj, d_sym_count, node_count, k,
+                                                                                   k_nn, d_out);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_query_batch(const ggnn_vectors* X, const ggnn_layer* bottom, const int32_t* d_top_rows, int64_t ntop,
+                     const ggnn_queries* Q, const ggnn_search_params* p, double d_nn1_max, int32_t* d_ids,
+                     double* d_dists, int32_t* d_counters, void* d_workspace, size_t workspace_bytes,
+                     void* stream) {
+  SearchArgs a;
+  int rc = fill_common(a, X, Q, p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(bottom && bottom->d_adj && bottom->k >= 1 && bottom->k <= MAX_K, "invalid bottom layer");
+  GGNN_CHECK_ARG(ntop >= 1, "the top layer is empty");
+  GGNN_CHECK_ARG(d_ids && d_dists, "null outputs");
+  a.layer = to_dev(*bottom);
+  a.top_rows = d_top_rows;
+  a.ntop = ntop;
+  a.dmax = d_nn1_max;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  a.counters = d_counters;
+  rc = attach_ever(a, p, p->k_out, bottom->k, d_workspace, workspace_bytes);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  switch (combo(X, Q)) {
+    case 0: return launch_warps(query_kernel<float, float>, a, a.m, a.region, st);
+    case 1: return launch_warps(query_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
+    default: return launch_warps(query_kernel<uint8_t, float>, a, a.m, a.region, st);
+  }
+}
+
+int ggnn_greedy_batch(const ggnn_vectors* X, const ggnn_layer* layer, const ggnn_queries* Q,
+                      const int32_t* d_seed_ids, const double* d_seed_dists, int32_t nseeds,
+                      const ggnn_search_params* p, double d_nn1_max, int32_t* d_ids, double* d_dists,
+                      int32_t* d_counters, void* d_workspace, size_t workspace_bytes, void* stream) {
+  SearchArgs a;
+  int rc = fill_common(a, X, Q, p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(layer && layer->d_adj && layer->k >= 1 && layer->k <= MAX_K, "invalid layer");
+  GGNN_CHECK_ARG(nseeds >= 1 && d_seed_ids && d_seed_dists, "greedy search needs at least one seed");
+  GGNN_CHECK_ARG(nseeds <= a.c.cap, "more seeds (%d) than cache capacity (%d)", nseeds, a.c.cap);
+  a.layer = to_dev(*layer);
+  a.dmax = d_nn1_max;
+  a.seed_ids = d_seed_ids;
+  a.seed_dists = d_seed_dists;
+  a.nseeds = nseeds;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  a.counters = d_counters;
+  rc = attach_ever(a, p, nseeds, layer->k, d_workspace, workspace_bytes);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  switch (combo(X, Q)) {
+    case 0: return launch_warps(greedy_kernel<float, float>, a, a.m, a.region, st);
+    case 1: return launch_warps(greedy_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
+    default: return launch_warps(greedy_kernel<uint8_t, float>, a, a.m, a.region, st);
+  }
+}
+
+int ggnn_descent_batch(const ggnn_vectors* X, const ggnn_layer* layers, int32_t num_layers, int32_t start,
+                       int32_t stop, const ggnn_queries* Q, const int32_t* d_seg_lo, const int32_t* d_seg_hi,
+                       const ggnn_search_params* p, int32_t* d_ids, double* d_dists, int32_t* d_counters,
+                       void* d_workspace, size_t workspace_bytes, void* stream) {
+  SearchArgs a;
+  int rc = fill_common(a, X, Q, p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(layers && num_layers >= 1 && num_layers <= MAX_LAYERS, "1..%d layers supported", MAX_LAYERS);
+  GGNN_CHECK_ARG(0 <= stop && stop <= start && start < num_layers, "invalid layer range %d..%d for %d layers",
+                 start, stop, num_layers);
+  for (int j = 0; j < num_layers; ++j) {
+    GGNN_CHECK_ARG(layers[j].k >= 1 && layers[j].k <= MAX_K, "invalid layer %d", j);
+    if (j > stop && j <= start) GGNN_CHECK_ARG(layers[j].d_down != nullptr, "layer %d needs a down map", j);
+    a.layers[j] = to_dev(layers[j]);
+  }
+  a.start = start;
+  a.stop = stop;
+  a.seg_lo = d_seg_lo;
+  a.seg_hi = d_seg_hi;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  a.counters = d_counters;
+  rc = attach_ever(a, p, p->k_out, MAX_K, d_workspace, workspace_bytes);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  switch (combo(X, Q)) {
+    case 0: return launch_warps(descent_kernel<float, float>, a, a.m, a.region, st);
+    case 1: return launch_warps(descent_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
+    default: return launch_warps(descent_kernel<uint8_t, float>, a, a.m, a.region, st);
+  }
+}
+
+int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const int32_t* d_x, const int32_t* d_z,
+                         const double* d_dxz, int64_t npairs, double tau, double d_nn1_max, int32_t budget,
+                         int32_t k_out, int32_t prioq_size, int32_t visited_size, int32_t n_fallback,
+                         int32_t* d_verdict, int32_t* d_fallback, void* stream) {
+  GGNN_CHECK_ARG(X && X->d_data && layer && layer->d_adj, "invalid arguments");
+  GGNN_CHECK_ARG(layer->k >= 1 && layer->k <= MAX_K, "k <= %d supported", MAX_K);
+  GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32 && n_fallback >= 0 && n_fallback <= 32, "k_out / n_fallback in [1, 32]");
+  if (npairs <= 0) return GGNN_OK;
+  SymArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = X->d_data;
+  a.d = X->d;
+  a.lpr = choose_lpr(X->d, X->dtype, X->dtype, reinterpret_cast<uintptr_t>(X->d_data));
+  a.layer = to_dev(*layer);
+  a.px = d_x;
+  a.pz = d_z;
+  a.pd = d_dxz;
+  a.npairs = npairs;
+  ggnn_search_params p{k_out, prioq_size, visited_size, 0, tau, budget};
+  a.c = make_cfg(&p);
+  a.dmax = d_nn1_max;
+  a.n_fallback = n_fallback;
+  a.verdict = d_verdict;
+  a.fallback = d_fallback;
+  int keysize = X->dtype == GGNN_U8 ? 4 : 8;
+  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
+  int W = pick_warps(a.region, 8);
+  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
+  size_t smem = (size_t)W * a.region;
+  cudaStream_t st = as_stream(stream);
+  int64_t grid = (npairs + W - 1) / W;
+  if (X->dtype == GGNN_U8) {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);
+  } else {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    symcheck_kernel<float><<<(unsigned)grid, W * 32, smem, st>>>(a);
+  }
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t nrows, const ggnn_queries* Q,
+                         int32_t k, int32_t* d_ids, double* d_dists, void* stream) {
+  ggnn_search_params p{k, 1, 1, 0, 0.0, 0};
+  SearchArgs a;
+  int rc = fill_common(a, X, Q, &p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(nrows >= 1 && nrows <= INT32_MAX, "invalid row count");
+  a.top_rows = d_rows;
+  a.ntop = nrows;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  int qd = Q->d_rows ? X->dtype : Q->dtype;
+  int keysize = (X->dtype == GGNN_U8 && qd == GGNN_U8) ? 4 : 8;
+  a.region = 128 + align16(32 * (size_t)keysize) + align16((size_t)X->d * qelem_of(qd));
+  cudaStream_t st = as_stream(stream);
+  switch (combo(X, Q)) {
+    case 0: return launch_warps(topk_kernel<float, float>, a, a.m, a.region, st, 8);
+    case 1: return launch_warps(topk_kernel<uint8_t, uint8_t>, a, a.m, a.region, st, 8);
+    default: return launch_warps(topk_kernel<uint8_t, float>, a, a.m, a.region, st, 8);
+  }
+}
+
+int ggnn_squared_l2_many(const ggnn_vectors* X, const ggnn_queries* Q, const int32_t* d_rows, int32_t per_query,
+                         double* d_out, void* stream) {
+  GGNN_CHECK_ARG(X && X->d_data && Q && d_rows && d_out && per_query >= 0, "invalid arguments");
+  int64_t total = Q->m * (int64_t)per_query;
+  if (total == 0) return GGNN_OK;
+  int qd = Q->d_rows ? X->dtype : Q->dtype;
+  unsigned grid = (unsigned)((total + 127) / 128);
+  cudaStream_t st = as_stream(stream);
+  if (X->dtype == GGNN_F32) {
+    sqdist_kernel<float, float><<<grid, 128, 0, st>>>((const float*)X->d_data, X->d, (const float*)Q->d_data,
+                                                      Q->d_rows, d_rows, per_query, total, d_out);
+  } else if (qd == GGNN_U8) {
+    sqdist_kernel<uint8_t, uint8_t><<<grid, 128, 0, st>>>((const uint8_t*)X->d_data, X->d,
+                                                          (const uint8_t*)Q->d_data, Q->d_rows, d_rows, per_query,
+                                                          total, d_out);
+  } else {
+    sqdist_kernel<uint8_t, float><<<grid, 128, 0, st>>>((const uint8_t*)X->d_data, X->d, (const float*)Q->d_data,
+                                                        Q->d_rows, d_rows, per_query, total, d_out);
+  }
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_f32_to_u8(const float* d_src, int64_t count, uint8_t* d_u8, int32_t* d_flag, void* stream) {
+  GGNN_CHECK_ARG(d_src && d_flag && count >= 0, "invalid arguments");
+  if (count == 0) return GGNN_OK;
+  DevInfo di = dev_info();
+  int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)std::max(di.sm_count, 1) * 8);
+  f32_to_u8_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(d_src, count, d_u8, d_flag);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+}  // extern "C"

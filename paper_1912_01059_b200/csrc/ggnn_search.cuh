@@ -1,0 +1,434 @@
+// ggnn_search.cuh -- one-warp-per-search best-first graph search.
+//
+// Restates the reference's `_greedy_core` (_core.pyx:190-311) with its search
+// cache (_core.pyx:135-176, cache.py:25-141) so that, on exact keys (uint8
+// data), ids / distances / visited_count / steps / terminated_by / forgotten
+// match the reference bit for bit.  The cache lives in
+// shared memory, one private region per warp:
+//
+//   rk[cap], rid[cap], rvis[cap]  the sorted ring (best-list + priority queue)
+//   vring[vsz]                    the visited ring (FIFO of expanded ids)
+//   ht[H]                         exact refcount table over ring u vring
+//   crow/cid/ckey[32]             per-step candidate scratch
+//   qs[d]                         the query vector
+//
+// One expansion step is executed warp-wide:
+//   head scan (ballot over visited bytes) -> threshold in FP64 -> adjacency row
+//   load (one coalesced 96-byte read for k=24) -> parallel refcount lookups +
+//   __match_any dedupe -> warp-cooperative 16-byte-vector distance gathers ->
+//   bitonic sort of the candidates -> threshold admission -> parallel merge
+//   into the ring (binary-search ranks, chunked right shift) with the exact
+//   eviction / visited-ring / refcount sequence of the sequential reference.
+#pragma once
+#include <climits>
+#include "ggnn_common.cuh"
+
+namespace ggnn {
+
+struct SearchCfg {
+  int k_out;
+  int cap;  // k_out + prioq_size
+  int vsz;  // visited ring size
+  int hlog; // log2 of the refcount table size
+  double tau;
+  long long max_steps;  // max_iterations, or the budget in found-target mode
+  int flags;
+};
+
+constexpr int FLAG_DISTINCT = 1;     // exact distinct_touched via a global set
+constexpr int FLAG_EXACT_DISTS = 2;  // re-score returned hits sequentially (bitwise _sqdist)
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Byte size of one warp's shared region.
+inline size_t warp_region_bytes(int cap, int vsz, int hlog, int64_t d, int qelem, int keysize) {
+  size_t b = 0;
+  b += align16((size_t)cap * keysize);      // rk
+  b += align16((size_t)cap * 4);            // rid
+  b += align16((size_t)((cap + 127) / 128) * 128);  // rvis (padded for 4-byte scans)
+  b += align16((size_t)vsz * 4);            // vring
+  b += align16((size_t)(1u << hlog) * 4);   // ht
+  b += 32 * 4 + 32 * 4 + align16(32 * (size_t)keysize);  // crow, cid, ckey
+  b += align16((size_t)d * qelem);          // qs
+  return b;
+}
+
+inline int table_log2(int cap, int vsz) {
+  int need = 2 * (cap + vsz);
+  int lg = 6;
+  while ((1 << lg) < need) ++lg;
+  return lg;
+}
+
+template <typename TX, typename TQ>
+struct WarpSearch {
+  using Key = typename VecTraits<TX, TQ>::Key;
+  using KO = KeyOps<Key>;
+
+  // data
+  const TX* X;
+  int64_t d;
+  int lpr;
+  TQ* qs;
+  // layer
+  const int32_t* adj;
+  int k;
+  const int32_t* to_row;  // nullptr = identity
+  double dmax;
+  // config
+  SearchCfg c;
+  int target;  // -1: normal mode
+  // shared memory
+  Key* rk;
+  int* rid;
+  uint8_t* rvis;
+  int* vring;
+  RefTable ht;
+  int* crow;
+  int* cid;
+  Key* ckey;
+  // diagnostic ever-set (global)
+  uint32_t* ever;
+  uint32_t ever_mask;
+  // warp-uniform state
+  int L, vlen, vpos, used;
+  int visited, steps, distinct, forgotten, term;
+
+  __device__ void carve(uint8_t* base) {
+    uint8_t* p = base;
+    rk = reinterpret_cast<Key*>(p);
+    p += align16((size_t)c.cap * sizeof(Key));
+    rid = reinterpret_cast<int*>(p);
+    p += align16((size_t)c.cap * 4);
+    rvis = p;
+    p += align16((size_t)((c.cap + 127) / 128) * 128);
+    vring = reinterpret_cast<int*>(p);
+    p += align16((size_t)c.vsz * 4);
+    ht.t = reinterpret_cast<uint32_t*>(p);
+    ht.mask = (1u << c.hlog) - 1u;
+    ht.shift = 32 - c.hlog;
+    p += align16((size_t)(1u << c.hlog) * 4);
+    crow = reinterpret_cast<int*>(p);
+    p += 32 * 4;
+    cid = reinterpret_cast<int*>(p);
+    p += 32 * 4;
+    ckey = reinterpret_cast<Key*>(p);
+    p += align16(32 * sizeof(Key));
+    qs = reinterpret_cast<TQ*>(p);
+  }
+
+  __device__ void reset() {
+    ht.clear();
+    L = vlen = vpos = used = 0;
+    visited = steps = distinct = forgotten = 0;
+    term = TERM_EMPTY;
+  }
+
+  __device__ __forceinline__ int ever_insert(int id) {
+    if (id < 0 || ever == nullptr) return 0;
+    uint32_t key = (uint32_t)id + 1u;
+    uint32_t s = (key * 2654435761u) & ever_mask;
+    for (;;) {
+      uint32_t v = ever[s];
+      if (v == key) return 0;
+      if (v == 0u) {
+        uint32_t o = atomicCAS(&ever[s], 0u, key);
+        if (o == 0u) return 1;
+        if (o == key) return 0;
+        continue;
+      }
+      s = (s + 1) & ever_mask;
+    }
+  }
+
+  __device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+  }
+
+  __device__ void rebuild() {
+    const int lane = lane_id();
+    ht.clear();
+    int u = 0;
+    for (int i = lane; i < L; i += 32) u += ht.add_one((uint32_t)rid[i]);
+    for (int i = lane; i < vlen; i += 32) u += ht.add_one((uint32_t)vring[i]);
+    used = warp_sum(u);
+    __syncwarp();
+  }
+
+  // ring position of the first unvisited entry, -1 if none
+  __device__ int head() const {
+    const int lane = lane_id();
+    for (int base = 0; base < L; base += 128) {
+      int p0 = base + 4 * lane;
+      uint32_t w = *reinterpret_cast<const uint32_t*>(rvis + p0);
+      int fb = 4;
+#pragma unroll
+      for (int b = 3; b >= 0; --b)
+        if (p0 + b < L && ((w >> (8 * b)) & 0xffu) == 0u) fb = b;
+      unsigned bal = __ballot_sync(FULL, fb < 4);
+      if (bal) {
+        int src = __ffs(bal) - 1;
+        return base + 4 * src + __shfl_sync(FULL, fb, src);
+      }
+    }
+    return -1;
+  }
+
+  __device__ void vring_push(int node) {
+    const int lane = lane_id();
+    if (vlen == c.vsz) {
+      int old = vring[vpos];
+      if (ht.dec((uint32_t)old)) forgotten++;
+      if (lane == 0) vring[vpos] = node;
+      vpos = (vpos + 1 == c.vsz) ? 0 : vpos + 1;
+    } else {
+      if (lane == 0) vring[vlen] = node;
+      vlen++;
+    }
+    __syncwarp();
+  }
+
+  // Lanes [0, m) hold ascending, distinct, currently-unknown (key, id) pairs.
+  // Equivalent to calling the reference's _ring_insert on each in order.
+  __device__ void merge(Key key, int id, int m) {
+    const int lane = lane_id();
+    int rank = 0;
+    if (lane < m) {
+      int lo = 0, hi = L;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        Key km = rk[mid];
+        if (km < key || (km == key && rid[mid] <= id))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      rank = lo;
+    }
+    const int p = rank + lane;
+    const bool ok = lane < m && p < c.cap;
+    const int madm = __popc(__ballot_sync(FULL, ok));
+    forgotten += m - madm;  // worse than the tail of a full ring
+    if (madm == 0) return;
+    const int newL = min(c.cap, L + madm);
+    const int E = L + madm - newL;
+    // evictions, largest first (_core.pyx:161-166)
+    for (int e = 0; e < E; ++e) {
+      const int r = L - 1 - e;
+      const int t = rid[r];
+      const bool vis = rvis[r] != 0;
+      if (vis) {
+        // push t onto the visited ring; its +1 and the ring's -1 cancel
+        vring_push(t);
+      } else {
+        ht.tomb((uint32_t)t);  // unvisited ring entries have count exactly 1
+        forgotten++;
+      }
+    }
+    // shift kept entries [rank_0, L-E) right by s_r = #{i : rank_i <= r}
+    const int Lkeep = L - E;
+    const int r0 = __shfl_sync(FULL, rank, 0);
+    for (int hi = Lkeep; hi > r0; hi -= 32) {
+      const int r = hi - 32 + lane;
+      const bool act = r >= r0;
+      Key kk = Key(0);
+      int ii = 0;
+      uint8_t vv = 0;
+      if (act) {
+        kk = rk[r];
+        ii = rid[r];
+        vv = rvis[r];
+      }
+      int s = 0;
+      for (int i = 0; i < madm; ++i) s += (__shfl_sync(FULL, rank, i) <= r) ? 1 : 0;
+      __syncwarp();
+      if (act) {
+        rk[r + s] = kk;
+        rid[r + s] = ii;
+        rvis[r + s] = vv;
+      }
+      __syncwarp();
+    }
+    if (ok) {
+      rk[p] = key;
+      rid[p] = id;
+      rvis[p] = 0;
+    }
+    int took = ok ? ht.insert_new((uint32_t)id) : 0;
+    used += warp_sum(took);
+    L = newL;
+    __syncwarp();
+    if (used > (int)((ht.mask + 1) >> 1)) rebuild();
+  }
+
+  // Seeds: lanes [0, n) hold (key, id) in the caller's order; duplicates and
+  // already-known ids are skipped (first occurrence wins), _core.pyx:219-229.
+  __device__ void seed(Key key, int id, int n) {
+    const int lane = lane_id();
+    bool v = lane < n && id >= 0;
+    if (v) v = ht.count((uint32_t)id) == 0u;
+    unsigned same = __match_any_sync(FULL, v ? (unsigned)id : (0x80000000u | (unsigned)lane));
+    v = v && ((same & lanemask_lt()) == 0u);
+    if (!v) {
+      key = KO::max_key();
+      id = INT_MAX;
+    }
+    const int cnt = __popc(__ballot_sync(FULL, v));
+    if (ever) distinct += warp_sum(ever_insert(v ? id : -1));
+    else distinct += cnt;
+    warp_sort(key, id);
+    if (cnt) merge(key, id, cnt);
+  }
+
+  // One expansion.  Returns false when the search has terminated.
+  __device__ bool step() {
+    const int lane = lane_id();
+    const int pos = head();
+    if (pos < 0) {
+      term = TERM_EMPTY;
+      return false;
+    }
+    double thr = __longlong_as_double(0x7ff0000000000000ll);
+    // FP64, rounded exactly like the reference (no FMA contraction):
+    // thr = ring[k_out-1] + tau * min(d_nn1_max, ring[0])   (_core.pyx:241-244)
+    if (L >= c.k_out) thr = __dadd_rn(KO::to_d(rk[c.k_out - 1]), __dmul_rn(c.tau, fmin(dmax, KO::to_d(rk[0]))));
+    if (KO::to_d(rk[pos]) > thr) {
+      term = TERM_STOP;
+      return false;
+    }
+    if ((long long)steps >= c.max_steps) {
+      term = TERM_CAP;
+      return false;
+    }
+    const int node = rid[pos];
+    __syncwarp();
+    if (lane == 0) rvis[pos] = 1;
+    vring_push(node);
+    ht.inc((uint32_t)node);
+
+    int nb = -1;
+    if (lane < k) nb = __ldg(adj + (int64_t)node * k + lane);
+    bool cand = nb >= 0;
+    if (cand) cand = ht.count((uint32_t)nb) == 0u;
+    unsigned same = __match_any_sync(FULL, cand ? (unsigned)nb : (0x80000000u | (unsigned)lane));
+    cand = cand && ((same & lanemask_lt()) == 0u);
+    const unsigned cm = __ballot_sync(FULL, cand);
+    const int nc = __popc(cm);
+    bool found = false;
+    if (nc) {
+      const int ci = __popc(cm & lanemask_lt());
+      if (cand) {
+        crow[ci] = to_row ? __ldg(to_row + nb) : nb;
+        cid[ci] = nb;
+      }
+      __syncwarp();
+      warp_dists<TX, TQ>(X, d, qs, crow, nc, ckey, lpr);
+      __syncwarp();
+      Key key = KO::max_key();
+      int id = INT_MAX;
+      if (lane < nc) {
+        key = ckey[lane];
+        id = cid[lane];
+      }
+      __syncwarp();
+      visited += nc;
+      if (ever) distinct += warp_sum(ever_insert(lane < nc ? id : -1));
+      warp_sort(key, id);
+      const bool adm = lane < nc && KO::to_d(key) <= thr;
+      const int m = __popc(__ballot_sync(FULL, adm));
+      forgotten += nc - m;
+      if (target >= 0) found = __any_sync(FULL, adm && id == target);
+      if (m) merge(key, id, m);
+    }
+    steps++;
+    if (found) {
+      term = 1;
+      return false;
+    }
+    return true;
+  }
+
+  __device__ void run() {
+    while (step()) {
+    }
+    if (target >= 0 && term != 1) term = 0;
+  }
+
+  // first min(L, k_out) ring entries -> ids / keys in lanes (k_out <= 32)
+  __device__ int hits(Key& key, int& id) const {
+    const int lane = lane_id();
+    const int nh = min(L, c.k_out);
+    key = KO::max_key();
+    id = -1;
+    if (lane < nh) {
+      key = rk[lane];
+      id = rid[lane];
+    }
+    return nh;
+  }
+};
+
+// Merge one unsorted chunk (ck, cx) (one pair per lane, invalid lanes hold
+// (max, INT_MAX)) into the running ascending top list (bk, bi), keeping the kk
+// smallest (kk <= 32).  The 32 smallest of two ascending lists is the
+// elementwise min against the reversed chunk (a bitonic sequence), which the
+// half-cleaners then sort.
+template <typename Key>
+__device__ __forceinline__ void topk_merge_chunk(Key& bk, int& bi, Key ck, int cx, int kk) {
+  using KO = KeyOps<Key>;
+  const int lane = lane_id();
+  warp_sort(ck, cx);
+  Key rk2 = KO::shfl(ck, 31 - lane);
+  int ri2 = __shfl_sync(FULL, cx, 31 - lane);
+  if (key_less(rk2, ri2, bk, bi)) {
+    bk = rk2;
+    bi = ri2;
+  }
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    Key ok = KO::shfl_xor(bk, stride);
+    int oi = __shfl_xor_sync(FULL, bi, stride);
+    bool lower = (lane & stride) == 0;
+    if (lower ? key_less(ok, oi, bk, bi) : key_less(bk, bi, ok, oi)) {
+      bk = ok;
+      bi = oi;
+    }
+  }
+  if (lane >= kk) {
+    bk = KO::max_key();
+    bi = INT_MAX;
+  }
+}
+
+// Exhaustive top-kk (kk <= 32) over rows[lo..hi) (or the index range itself
+// when rows is null), ties by local index; the result sits in lanes [0, kk)
+// as (key, local index) -- the reference's exhaustive_topk (_core.pyx:86-104).
+template <typename TX, typename TQ>
+__device__ void warp_topk_scan(const TX* X, int64_t d, const TQ* qs, int lpr, const int32_t* rows, int lo, int hi,
+                               int kk, int* crow, typename VecTraits<TX, TQ>::Key* ckey,
+                               typename VecTraits<TX, TQ>::Key& bk, int& bi) {
+  using Key = typename VecTraits<TX, TQ>::Key;
+  using KO = KeyOps<Key>;
+  const int lane = lane_id();
+  bk = KO::max_key();
+  bi = INT_MAX;
+  for (int base = lo; base < hi; base += 32) {
+    const int cnt = min(32, hi - base);
+    if (lane < cnt) crow[lane] = rows ? __ldg(rows + base + lane) : base + lane;
+    __syncwarp();
+    warp_dists<TX, TQ>(X, d, qs, crow, cnt, ckey, lpr);
+    __syncwarp();
+    Key ck = KO::max_key();
+    int cx = INT_MAX;
+    if (lane < cnt) {
+      ck = ckey[lane];
+      cx = base + lane - lo;
+    }
+    __syncwarp();
+    topk_merge_chunk(bk, bi, ck, cx, kk);
+  }
+}
+
+}  // namespace ggnn

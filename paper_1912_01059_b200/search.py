@@ -1,0 +1,226 @@
+"""Greedy best-first graph search on the GPU (drop-in for graphann.search).
+
+API and result types follow /root/reference/pkg/src/graphann/search.py; each
+call is one batched kernel launch (ggnn_query_batch / ggnn_greedy_batch /
+ggnn_descent_batch) instead of the reference's per-query C call.  All
+distances are squared L2; tau is applied in squared space (search.py:45-54).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .config import QueryConfig
+from .device import DeviceVectors, device_hierarchy
+
+TERMINATED_BY = {0: "stopping-rule", 1: "queue-empty", 2: "iteration-cap"}
+_TERM_CODE = {v: k for k, v in TERMINATED_BY.items()}
+
+# queries per launch when exact distinct_touched is requested (its per-query
+# diagnostic set lives in device workspace)
+_DISTINCT_CHUNK = 512
+
+
+@dataclass
+class QueryResult:
+    """Ascending (id, distance) results plus search-effort diagnostics."""
+
+    ids: np.ndarray
+    dists: np.ndarray
+    visited_count: int
+    steps: int
+    terminated_by: str
+    distinct_touched: int = 0
+    forgotten: int = 0
+
+    @property
+    def hits(self) -> list[tuple[int, float]]:
+        return [(int(i), float(d)) for i, d in zip(self.ids, self.dists)]
+
+
+def stopping_check(d_next: float, d_best_k: float, d_best_1: float, d_nn1_max: float, tau: float) -> bool:
+    """True when the closest unvisited candidate lies beyond the slack
+    d_best_k + tau * min(d_nn1_max, d_best_1); strict (search.py:45-54).
+    The device kernel evaluates the same expression in FP64."""
+    return bool(d_next > d_best_k + tau * min(d_nn1_max, d_best_1))
+
+
+@dataclass
+class BatchResult:
+    """Array form of a query batch: ids / dists (m, k_out), -1 / inf padded;
+    counters (m, 5) = visited, steps, term code, distinct, forgotten."""
+
+    ids: np.ndarray
+    dists: np.ndarray
+    counters: np.ndarray
+
+    def results(self) -> list[QueryResult]:
+        out = []
+        for i in range(self.ids.shape[0]):
+            nh = int((self.ids[i] >= 0).sum())
+            c = self.counters[i]
+            out.append(QueryResult(self.ids[i, :nh].copy(), self.dists[i, :nh].copy(), int(c[0]), int(c[1]),
+                                   TERMINATED_BY[int(c[2])], int(c[3]), int(c[4])))
+        return out
+
+
+def _params(cfg: QueryConfig, flags: int):
+    return N.search_params(cfg.k_out, cfg.prioq_size, cfg.visited_size, cfg.tau, cfg.max_iterations, flags)
+
+
+def _flags(dv: DeviceVectors, distinct: bool) -> int:
+    f = 0 if dv.exact_integers else N.FLAG_EXACT_DISTS
+    return f | (N.FLAG_DISTINCT if distinct else 0)
+
+
+def _workspace(m, params, max_seeds):
+    nbytes = N.load().ggnn_search_workspace_bytes(m, N.ctypes.byref(params), max_seeds)
+    if not nbytes:
+        return None, 0
+    return N.empty((nbytes,), N.torch().uint8), nbytes
+
+
+def _check_query(h, q: np.ndarray) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    if q.ndim != 1 or (h.dim and q.shape[0] != h.dim):
+        raise ValueError(f"query shape {q.shape} does not match index dimension {h.dim}")
+    return q
+
+
+def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinct: bool = False,
+                 out: str = "numpy"):
+    """Batched query(): top-layer scan + best-first search on layer 0 for every
+    row of `queries` in one launch.  Returns a BatchResult (host arrays) or,
+    with out="device", the device tensors (ids, dists, counters)."""
+    cfg = cfg or QueryConfig()
+    dh = device_hierarchy(h)
+    dv = dh.vectors
+    Q = np.ascontiguousarray(queries, dtype=np.float32)
+    if Q.ndim == 1:
+        Q = Q[None, :]
+    if Q.shape[1] != dv.d:
+        raise ValueError(f"query dimension {Q.shape[1]} does not match index dimension {dv.d}")
+    m = Q.shape[0]
+    t = N.torch()
+    ids = N.empty((m, cfg.k_out), t.int32)
+    dists = N.empty((m, cfg.k_out), t.float64)
+    cnt = N.empty((m, 5), t.int32)
+    params = _params(cfg, _flags(dv, distinct))
+    chunk = _DISTINCT_CHUNK if distinct else max(m, 1)
+    dq, qs = dv.queries(Q)
+    bottom = dh.layers[0]
+    for lo in range(0, m, chunk):
+        hi = min(m, lo + chunk)
+        sub = N.Queries(N.P(dq.data_ptr() + lo * Q.shape[1] * dq.element_size()), None, hi - lo, qs.dtype, 0)
+        ws, wsb = _workspace(hi - lo, params, cfg.k_out)
+        N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(bottom.struct), N.ptr(dh.top_rows),
+               dh.ntop, N.ctypes.byref(sub), N.ctypes.byref(params), dh.d_nn1_max, N.P(ids.data_ptr() + lo * 4 * cfg.k_out),
+               N.P(dists.data_ptr() + lo * 8 * cfg.k_out), N.P(cnt.data_ptr() + lo * 20), N.ptr(ws), wsb,
+               N.stream_ptr())
+    if out == "device":
+        return ids, dists, cnt
+    return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())
+
+
+def query(h, q: np.ndarray, cfg: QueryConfig | None = None) -> QueryResult:
+    """Top-to-bottom jump: brute-force the top layer, then search the bottom
+    (search.py:115-137)."""
+    q = _check_query(h, q)
+    return query_arrays(h, q[None, :], cfg, distinct=True).results()[0]
+
+
+def batch_query(h, queries: np.ndarray, cfg: QueryConfig | None = None, threads: int = 1) -> list[QueryResult]:
+    """Independent queries, one GPU launch per batch (search.py:213-226).
+    `threads` is accepted for signature compatibility and ignored."""
+    queries = np.ascontiguousarray(queries, dtype=np.float32)
+    if queries.ndim != 2 or (h.dim and queries.shape[1] != h.dim):
+        raise ValueError(f"query shape {queries.shape} does not match index dimension {h.dim}")
+    if queries.shape[0] == 0:
+        return []
+    return query_arrays(h, queries, cfg, distinct=True).results()
+
+
+def top_layer_seeds(h, q: np.ndarray, k_out: int):
+    """Exact top-min(k_out, |top|) of the top layer as dataset ids, plus the
+    number of distances spent (search.py:100-112)."""
+    from . import backend
+
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    top = h.num_layers - 1
+    rows = h.rows_for(top)
+    local, dists = backend.impl.exhaustive_topk_rows(h.dataset, rows, q, min(k_out, len(rows)))
+    return rows[local].astype(np.int32), dists, len(rows)
+
+
+def greedy_search(X: np.ndarray, to_row: np.ndarray, layer, seed_ids, seed_dists, q: np.ndarray, cfg: QueryConfig,
+                  d_nn1_max: float) -> QueryResult:
+    """Best-first search on one layer from precomputed seeds
+    (search.py:57-97)."""
+    from . import backend
+
+    seed_ids = np.asarray(seed_ids, dtype=np.int32)
+    seed_dists = np.asarray(seed_dists, dtype=np.float64)
+    if seed_ids.size == 0:
+        raise ValueError("greedy search needs at least one seed")
+    if seed_ids.min() < 0 or seed_ids.max() >= layer.node_count:
+        raise ValueError("seed id out of range for this layer")
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    ids, dists, visited, steps, term, distinct, forgotten = backend.impl.greedy_search(
+        X, to_row, layer.adjacency, layer.k_nn, layer.sym_count, q, seed_ids, seed_dists, cfg.k_out, cfg.tau,
+        d_nn1_max, cfg.max_iterations, cfg.prioq_size, cfg.visited_size)
+    return QueryResult(ids, dists, visited, steps, TERMINATED_BY[term], distinct, forgotten)
+
+
+def hierarchical_query(h, q: np.ndarray, cfg: QueryConfig | None = None, start_layer: int | None = None,
+                       stop_layer: int = 0, segment: tuple[int, int] | None = None,
+                       slack_bounds: list[float] | None = None, segment_cache: dict | None = None) -> QueryResult:
+    """Layer-by-layer descent (search.py:140-210): brute-force the start
+    layer (or one segment of it), then seed each finer layer's greedy search
+    with the previous layer's k_out hits.  `segment_cache` is accepted for
+    signature compatibility; the device keeps everything resident."""
+    cfg = cfg or QueryConfig()
+    q = _check_query(h, q)
+    start = h.num_layers - 1 if start_layer is None else start_layer
+    if not (0 <= stop_layer <= start < h.num_layers):
+        raise ValueError(f"invalid layer range {start}..{stop_layer} for {h.num_layers} layers")
+    lo, hi = segment if segment is not None else (0, h.layers[start].node_count)
+    res = descent_arrays(h, q[None, :], cfg, start, stop_layer, np.array([lo], dtype=np.int32),
+                         np.array([hi], dtype=np.int32), slack_bounds, distinct=True)
+    return res.results()[0]
+
+
+def descent_arrays(h, queries, cfg: QueryConfig, start: int, stop: int, seg_lo=None, seg_hi=None,
+                   slack_bounds=None, distinct: bool = False, query_rows=None) -> BatchResult:
+    """Batched hierarchical_query.  With `query_rows` (device int32) the
+    queries are dataset rows (construction-time self queries)."""
+    dh = device_hierarchy(h)
+    dv = dh.vectors
+    t = N.torch()
+    layers = dh.layer_array()
+    for j in range(dh.num_layers):
+        if slack_bounds is not None:
+            layers[j].slack = float(slack_bounds[j])
+        elif j == 0:
+            layers[j].slack = float(dh.d_nn1_max)
+    if query_rows is not None:
+        m = int(query_rows.shape[0])
+        qs = N.queries_struct(rows=query_rows, dtype_code=dv.dtype)
+        keep = query_rows
+    else:
+        keep, qs = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
+        m = qs.m
+    lo_d = N.to_dev(np.asarray(seg_lo, dtype=np.int32)) if seg_lo is not None else None
+    hi_d = N.to_dev(np.asarray(seg_hi, dtype=np.int32)) if seg_hi is not None else None
+    ids = N.empty((m, cfg.k_out), t.int32)
+    dists = N.empty((m, cfg.k_out), t.float64)
+    cnt = N.empty((m, 5), t.int32)
+    params = _params(cfg, _flags(dv, distinct))
+    ws, wsb = _workspace(m, params, cfg.k_out)
+    N.call("ggnn_descent_batch", N.ctypes.byref(dv.struct), layers, dh.num_layers, start, stop, N.ctypes.byref(qs),
+           N.ptr(lo_d), N.ptr(hi_d), N.ctypes.byref(params), N.ptr(ids), N.ptr(dists), N.ptr(cnt), N.ptr(ws), wsb,
+           N.stream_ptr())
+    del keep
+    return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())

@@ -1,0 +1,64 @@
+"""Seeded synthetic datasets of the benchmark shapes (BASELINE.json configs).
+
+Two generators, both integer-valued in [0, 255] so that float32 squared
+distances (and the device's lossless uint8 copy) are exact:
+
+* ``make_sift_shaped`` -- the reference test-suite's SIFT stand-in ("G_A"),
+  restated from /root/reference/pkg/tests/conftest.py:79-87.
+* ``make_latent16``    -- the low-intrinsic-dimension SIFT analogue ("G_B")
+  defined in SURVEY.md section 8(d); for n >= 1M rows it is generated in
+  chunks of 1M rows with seed (seed, chunk) so that memory stays bounded.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def make_sift_shaped(n=10000, d=128, m=100, seed=1234):
+    """Integer-valued clustered vectors mimicking SIFT descriptor scale."""
+    rng = np.random.default_rng(seed)
+    centers = rng.uniform(30, 225, size=(64, d))
+    assign = rng.integers(0, 64, size=n)
+    base = np.clip(np.rint(centers[assign] + rng.normal(0, 12, (n, d))), 0, 255)
+    picks = rng.choice(n, size=m, replace=False)
+    queries = np.clip(np.rint(base[picks] + rng.normal(0, 12, (m, d))), 0, 255)
+    return base.astype(np.float32), queries.astype(np.float32)
+
+
+def _latent_draw(rng, A, C, k, d, as_float):
+    z = C[rng.integers(0, 64, size=k)] + 0.6 * rng.standard_normal((k, 16))
+    x = 128.0 + 28.0 * (z @ A) + rng.normal(0, 2, (k, d))
+    if as_float:
+        return (np.clip(x, 0, 255) / 255.0).astype(np.float32)
+    return np.clip(np.rint(x), 0, 255).astype(np.float32)
+
+
+CHUNK = 1_000_000
+
+
+def make_latent16(n=10000, d=128, m=1000, seed=1234, as_float=False):
+    """G_B ("latent16"): base (n, d) then queries (m, d), float32.
+
+    as_float=True gives the GIST-like float variant (no rint, divided by 255)
+    used for the d=960 configuration.
+    """
+    if n <= CHUNK:
+        rng = np.random.default_rng(seed)
+        A = rng.standard_normal((16, d)) / 4.0
+        C = rng.standard_normal((64, 16)) * 2.0
+        base = _latent_draw(rng, A, C, n, d, as_float)
+        queries = _latent_draw(rng, A, C, m, d, as_float)
+        return base, queries
+    # chunked canonical stream: shared (A, C) from `seed`, rows from (seed, chunk)
+    rng0 = np.random.default_rng(seed)
+    A = rng0.standard_normal((16, d)) / 4.0
+    C = rng0.standard_normal((64, 16)) * 2.0
+    base = np.empty((n, d), dtype=np.float32)
+    for c, lo in enumerate(range(0, n, CHUNK)):
+        hi = min(n, lo + CHUNK)
+        rng = np.random.default_rng((seed, c))
+        base[lo:hi] = _latent_draw(rng, A, C, hi - lo, d, as_float)
+    rngq = np.random.default_rng((seed, 0x51E7))
+    queries = _latent_draw(rngq, A, C, m, d, as_float)
+    return base, queries

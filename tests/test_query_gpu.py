@@ -1,0 +1,180 @@
+"""GPU query path vs the reference (golden fixtures) and the CPU checker.
+
+Bar (BASELINE.json north_star):
+  * integer data (exact distances): ids, float64 distances, visited_count,
+    steps, terminated_by, distinct_touched and forgotten identical;
+  * float data: first-hit agreement >= 49/50 and matching distances within
+    rtol 1e-9 (the reference's own float tolerance, test_backends.py:97-111),
+    returned distances bitwise equal to squared_distance.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1912_01059_b200 as ga
+from conftest import TERM_CODE, golden_hierarchy, oracle_layers
+
+pytestmark = pytest.mark.gpu
+
+
+def _as_table(results, k):
+    ids = np.full((len(results), k), -1, dtype=np.int32)
+    dists = np.full((len(results), k), np.inf)
+    cnt = np.zeros((len(results), 5), dtype=np.int64)
+    for i, r in enumerate(results):
+        ids[i, : len(r.ids)] = r.ids
+        dists[i, : len(r.dists)] = r.dists
+        cnt[i] = [r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten]
+    return ids, dists, cnt
+
+
+@pytest.mark.parametrize("tag", ["q_default", "q_tiny", "q_cap"])
+def test_golden_int_queries_bitwise(golden_int, tag):
+    g, h = golden_int
+    k_out, max_it, prioq, vis = (int(v) for v in g[tag + "_cfg"])
+    cfg = ga.QueryConfig(k_out=k_out, tau=float(g[tag + "_tau"]), max_iterations=max_it, prioq_size=prioq,
+                         visited_size=vis)
+    ids, dists, cnt = _as_table(ga.batch_query(h, g["Q"], cfg), k_out)
+    np.testing.assert_array_equal(ids, g[tag + "_ids"])
+    np.testing.assert_array_equal(dists, g[tag + "_dists"])
+    np.testing.assert_array_equal(cnt, g[tag + "_cnt"])
+
+
+def test_golden_sift10k_bitwise(golden_sift):
+    g, h, Q = golden_sift
+    for tag, tau in (("q3", 0.3), ("q6", 0.6), ("q8", 0.8)):
+        ids, dists, cnt = _as_table(ga.batch_query(h, Q, ga.QueryConfig(k_out=10, tau=tau)), 10)
+        np.testing.assert_array_equal(ids, g[tag + "_ids"])
+        np.testing.assert_array_equal(dists, g[tag + "_dists"])
+        np.testing.assert_array_equal(cnt, g[tag + "_cnt"])
+
+
+def test_golden_greedy_from_seeds(golden_int):
+    g, h = golden_int
+    X = g["X"]
+    cfg = ga.QueryConfig(k_out=6, tau=0.4, max_iterations=1000, prioq_size=12, visited_size=16)
+    for i in range(len(g["Q"])):
+        seeds = g["gs_seeds"][i]
+        sd = np.array([O.squared_l2(g["Q"][i], X[s]) for s in seeds])
+        r = ga.greedy_search(h.vectors(), h.rows_for(0), h.layers[0], seeds, sd, g["Q"][i], cfg, h.stats.d_nn1_max)
+        nh = len(r.ids)
+        np.testing.assert_array_equal(r.ids, g["gs_ids"][i, :nh])
+        np.testing.assert_array_equal(r.dists, g["gs_d"][i, :nh])
+        got = (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten)
+        assert got == tuple(int(v) for v in g["gs_cnt"][i])
+
+
+def test_golden_kernels(golden_int):
+    g, h = golden_int
+    impl = ga.backend.impl
+    X = g["X"]
+    for i, q in enumerate(g["Q"][:20]):
+        ids, d = impl.exhaustive_topk(X, q, 9)
+        np.testing.assert_array_equal(ids, g["topk_ids"][i])
+        np.testing.assert_array_equal(d, g["topk_d"][i])
+    for b in range(4):
+        pos, dist = impl.batch_bruteforce(X, g[f"bb_mem{b}"], 6)
+        np.testing.assert_array_equal(pos, g[f"bb_pos{b}"])
+        np.testing.assert_array_equal(dist, g[f"bb_dist{b}"])
+    L = h.layers[0]
+    sc = impl.SymScratch(L.node_count, L.k, 68, 128, 16, 8)
+    for (x, z), v, fb in zip(g["sym_pairs"][:120], g["sym_verdict"][:120], g["sym_fb"][:120]):
+        got_v, got_fb = impl.sym_check_pair(X, h.rows_for(0), L.adjacency, L.k_nn, L.sym_count, int(x), int(z),
+                                            O.squared_l2(X[x], X[z]), 0.5, L.live_d_nn1_max(), 16, 4, 64, 128, 8, sc)
+        assert got_v == v
+        if v == 2:
+            np.testing.assert_array_equal(got_fb, fb)
+
+
+def test_golden_float_tolerance(golden_float):
+    g, h = golden_float
+    res = ga.batch_query(h, g["Q"], ga.QueryConfig(k_out=5, tau=0.6))
+    same_first = 0
+    for i, r in enumerate(res):
+        same_first += int(r.ids[0] == g["q_ids"][i, 0])
+        if np.array_equal(r.ids, g["q_ids"][i, : len(r.ids)]):
+            np.testing.assert_allclose(r.dists, g["q_dists"][i, : len(r.dists)], rtol=1e-9)
+        for node, dist in r.hits:
+            assert O.squared_l2(g["Q"][i], g["X"][node]) == dist  # bitwise sequential FP64
+    assert same_first >= 49
+
+
+def _random_int_hierarchy(seed, n=1500, d=16):
+    """A reference-shaped graph built by the checker-composed pipeline is not
+    available on the GPU box, so build a valid layered graph directly: an
+    exact kNN bottom (oracle brute force) plus random inverse links and a
+    random top layer."""
+    rng = np.random.default_rng(seed)
+    X = rng.integers(0, 256, size=(n, d)).astype(np.float32)
+    k, k_nn = 8, 4
+    pos, dist = O.batch_bruteforce(X, np.arange(n, dtype=np.int32), k_nn)
+    layer = ga.AdjacencyLayer(n, k, k_nn)
+    layer.adjacency[:, :k_nn] = pos
+    layer.nn_dists[:] = dist
+    layer.d_nn1[:] = dist[:, 0]
+    symc = rng.integers(0, k - k_nn + 1, size=n)
+    for i in range(n):
+        cand = [int(c) for c in rng.choice(n, size=int(symc[i]) + 4, replace=False) if c != i and c not in pos[i]]
+        cand = cand[: int(symc[i])]
+        layer.adjacency[i, k_nn : k_nn + len(cand)] = cand
+        layer.sym_count[i] = len(cand)
+    top_rows = np.sort(rng.choice(n, size=32, replace=False)).astype(np.int32)
+    top = ga.AdjacencyLayer(32, k, k_nn)
+    cfg = ga.BuildConfig(k=k, k_nn=k_nn, k_sym=k - k_nn, s=32, g=2, seed=0)
+    h = ga.Hierarchy([layer, top], [None, top_rows], 32, 2, cfg,
+                     ga.GraphStats(float(dist[:, 0].mean()), float(dist[:, 0].max())), dim=d)
+    h.attach(ga.Dataset(X))
+    return h, rng
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_int_graphs_vs_checker(seed):
+    h, rng = _random_int_hierarchy(seed)
+    Q = rng.integers(0, 256, size=(300, h.dim)).astype(np.float32)
+    for cfg in (ga.QueryConfig(k_out=10, tau=0.6), ga.QueryConfig(k_out=4, tau=1.5, prioq_size=8, visited_size=5),
+                ga.QueryConfig(k_out=7, tau=0.0, max_iterations=3, prioq_size=20, visited_size=40),
+                ga.QueryConfig(k_out=32, tau=0.8, prioq_size=64, visited_size=600)):
+        got = ga.batch_query(h, Q, cfg)
+        for q, r in zip(Q, got):
+            want = O.query(oracle_layers(h), h.to_bottom, h.vectors(), q, cfg.k_out, cfg.tau, h.stats.d_nn1_max,
+                           cfg.max_iterations, cfg.prioq_size, cfg.visited_size)
+            np.testing.assert_array_equal(r.ids, want[0])
+            np.testing.assert_array_equal(r.dists, want[1])
+            assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched,
+                    r.forgotten) == tuple(want[2:])
+
+
+def test_query_arrays_matches_batch_query(golden_sift):
+    g, h, Q = golden_sift
+    cfg = ga.QueryConfig(k_out=10, tau=0.6)
+    arr = ga.query_arrays(h, Q, cfg)
+    np.testing.assert_array_equal(arr.ids, g["q6_ids"])
+    np.testing.assert_array_equal(arr.dists, g["q6_dists"])
+    np.testing.assert_array_equal(arr.counters[:, [0, 1, 2, 4]], g["q6_cnt"][:, [0, 1, 2, 4]])
+
+
+def test_hierarchical_query_matches_checker(golden_int):
+    g, h = golden_int
+    cfg = ga.QueryConfig(k_out=5, tau=0.6)
+    X = h.vectors()
+    for q in g["Q"][:40]:
+        r = ga.hierarchical_query(h, q, cfg)
+        # checker composition of search.py:140-210
+        top = h.num_layers - 1
+        rows = h.rows_for(top)
+        local, dists = O.exhaustive_topk(X[rows], q, min(cfg.k_out, len(rows)))
+        ids = local.astype(np.int32)
+        v, t, dist_cnt, fg, term = len(rows), 0, len(rows) - len(ids), 0, 1
+        for j in range(top - 1, -1, -1):
+            seeds = h.local_ids(j, h.rows_for(j + 1)[ids])
+            L = h.layers[j]
+            bound = h.stats.d_nn1_max if j == 0 else L.live_d_nn1_max()
+            ids, dists, nv, nt, term, nd, nf = O.greedy_search(X, h.rows_for(j), L.adjacency, L.k_nn, L.sym_count,
+                                                               q, seeds, dists, cfg.k_out, cfg.tau, bound,
+                                                               cfg.max_iterations, cfg.prioq_size, cfg.visited_size)
+            v, t, dist_cnt, fg = v + nv, t + nt, dist_cnt + nd, fg + nf
+        np.testing.assert_array_equal(r.ids, ids)
+        np.testing.assert_array_equal(r.dists, dists)
+        assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten) == (
+            v, t, term, dist_cnt, fg)
