@@ -77,6 +77,11 @@ struct SearchArgs {
   int start, stop;
   const int32_t* seg_lo;
   const int32_t* seg_hi;
+  // computed segments (construction): seg = (seg_of ? seg_of[i] : i) / seg_div,
+  // rows [seg * seg_size, seg * seg_size + seg_size) of the start layer
+  const int32_t* seg_of;
+  int seg_div;
+  int seg_size;
 };
 
 template <typename TX, typename TQ>
@@ -226,8 +231,13 @@ __global__ void __launch_bounds__(256) descent_kernel(const __grid_constant__ Se
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   const LayerDev& Ls = a.layers[a.start];
-  const int lo = a.seg_lo ? __ldg(a.seg_lo + qi) : 0;
-  const int hi = a.seg_hi ? __ldg(a.seg_hi + qi) : (int)Ls.node_count;
+  int lo = a.seg_lo ? __ldg(a.seg_lo + qi) : 0;
+  int hi = a.seg_hi ? __ldg(a.seg_hi + qi) : (int)Ls.node_count;
+  if (a.seg_size > 0) {
+    const int seg = (a.seg_of ? __ldg(a.seg_of + qi) : (int)qi) / a.seg_div;
+    lo = seg * a.seg_size;
+    hi = min(lo + a.seg_size, (int)Ls.node_count);
+  }
   const int kk = min(a.c.k_out, hi - lo);
   Key bk;
   int bi;
@@ -292,6 +302,17 @@ struct SymArgs {
   int n_fallback;
   int32_t* verdict;
   int32_t* fallback;
+  // layer-pairs mode (px == nullptr): pair p = x * per_node + t, t < k_nn is
+  // direct slot t of x (adj / nnd), t >= k_nn the (t - k_nn)-th rescued entry
+  const double* nnd;
+  int k_nn;
+  const int32_t* resc_id;
+  const double* resc_d;
+  int per_node;
+  // compact verdict-2 output: req[i] = {pair index, x, z, fb[n_fallback]}
+  int32_t* req;
+  int32_t* req_count;
+  int64_t req_cap;
 };
 
 template <typename TX>
@@ -302,14 +323,36 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
   const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (pi >= a.npairs) return;
   const int lane = lane_id();
-  const int x = __ldg(a.px + pi), z = __ldg(a.pz + pi);
+  int x, z;
+  double dxz;
+  if (a.px) {
+    x = __ldg(a.px + pi);
+    z = __ldg(a.pz + pi);
+    dxz = a.pd[pi];
+  } else {
+    x = (int)(pi / a.per_node);
+    const int t = (int)(pi - (int64_t)x * a.per_node);
+    if (t < a.k_nn) {
+      z = __ldg(a.layer.adj + (int64_t)x * a.layer.k + t);
+      dxz = z >= 0 ? a.nnd[(int64_t)x * a.k_nn + t] : 0.0;
+    } else {
+      const int64_t r = (int64_t)x * (a.per_node - a.k_nn) + (t - a.k_nn);
+      z = a.resc_id ? __ldg(a.resc_id + r) : -1;
+      dxz = z >= 0 ? a.resc_d[r] : 0.0;
+    }
+  }
+  int32_t* fb = a.fallback ? a.fallback + pi * a.n_fallback : nullptr;
+  if (z < 0) {  // empty slot: nothing to check
+    if (lane == 0 && a.verdict) a.verdict[pi] = -1;
+    return;
+  }
   // verdict 0: x already sits in one of z's slots (_core.pyx:405-408)
   int slot = lane < a.layer.k ? __ldg(a.layer.adj + (int64_t)z * a.layer.k + lane) : -1;
   const bool present = __any_sync(FULL, slot == x);
-  int32_t* fb = a.fallback + pi * a.n_fallback;
   if (present) {
-    if (lane == 0) a.verdict[pi] = 0;
-    for (int j = lane; j < a.n_fallback; j += 32) fb[j] = -1;
+    if (lane == 0 && a.verdict) a.verdict[pi] = 0;
+    if (fb)
+      for (int j = lane; j < a.n_fallback; j += 32) fb[j] = -1;
     return;
   }
   WarpSearch<TX, TX> s;
@@ -328,20 +371,42 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
   for (int64_t e = lane; e < a.d; e += 32) s.qs[e] = src[e];
   __syncwarp();
   s.reset();
-  s.seed(KeyOps<Key>::from_d(a.pd[pi]), lane == 0 ? z : -1, 1);
+  s.seed(KeyOps<Key>::from_d(dxz), lane == 0 ? z : -1, 1);
   s.run();
   const int v = s.term ? 1 : 2;
-  if (lane == 0) a.verdict[pi] = v;
+  if (lane == 0 && a.verdict) a.verdict[pi] = v;
+  if (v != 2) {
+    if (fb)
+      for (int j = lane; j < a.n_fallback; j += 32) fb[j] = -1;
+    return;
+  }
   // fallbacks: closest explored ids excluding x and z (_core.pyx:420-426)
   int cand = -1;
   const int nh = min(s.L, a.c.k_out);
-  if (v == 2 && lane < nh) cand = s.rid[lane];
+  if (lane < nh) cand = s.rid[lane];
   const bool keep = cand >= 0 && cand != x && cand != z;
   const unsigned km = __ballot_sync(FULL, keep);
   const int rank = __popc(km & lanemask_lt());
-  if (keep && rank < a.n_fallback) fb[rank] = cand;
   const int w = min(__popc(km), a.n_fallback);
-  for (int j = w + lane; j < a.n_fallback; j += 32) fb[j] = -1;
+  if (fb) {
+    if (keep && rank < a.n_fallback) fb[rank] = cand;
+    for (int j = w + lane; j < a.n_fallback; j += 32) fb[j] = -1;
+  }
+  if (a.req) {
+    int slot_i = 0;
+    if (lane == 0) slot_i = atomicAdd(a.req_count, 1);
+    slot_i = __shfl_sync(FULL, slot_i, 0);
+    if (slot_i < a.req_cap) {
+      int32_t* r = a.req + (int64_t)slot_i * (3 + a.n_fallback);
+      if (lane == 0) {
+        r[0] = (int32_t)pi;
+        r[1] = x;
+        r[2] = z;
+      }
+      if (keep && rank < a.n_fallback) r[3 + rank] = cand;
+      for (int j = w + lane; j < a.n_fallback; j += 32) r[3 + j] = -1;
+    }
+  }
 }
 
 // ----------------------------------------------------------- exhaustive_topk
