@@ -26,6 +26,56 @@ int ggnn_leaf_knn(const ggnn_vectors *X, const int32_t *d_nodes, const int32_t *
                   int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t *d_pos, double *d_dist, int32_t *d_adj,
                   int32_t k, double *d_nnd, double *d_dnn1, int32_t *d_reduced, void *stream);
 
+/* Replaces: the per-node hierarchical_query calls of merge_layer
+ * (build.py:146-197, search.py:140-210) for all m nodes of layer `stop` at
+ * once.  Query i is base row d_query_rows[i]; it brute-forces the segment
+ * seg = (d_seg_of ? d_seg_of[i] : i) / seg_div, i.e. rows
+ * [seg * seg_size, (seg + 1) * seg_size) of layer `start`, then descends to
+ * `stop` (each layer's slack = its frozen live_d_nn1_max).  Outputs are
+ * stop-layer local ids / distances (m, k_out) and optional counters (m, 5). */
+int ggnn_merge_descent(const ggnn_vectors *X, const ggnn_layer *layers, int32_t num_layers, int32_t start,
+                       int32_t stop, const int32_t *d_query_rows, int64_t m, const int32_t *d_seg_of, int32_t seg_div,
+                       int32_t seg_size, const ggnn_search_params *p, int32_t *d_ids, double *d_dists,
+                       int32_t *d_counters, void *stream);
+
+/* Replaces: AdjacencyLayer.merge_hits (graph.py:121-165) applied to every
+ * node of a layer: d_hit_ids / d_hit_dists (node_count, hits_per_node) are the
+ * node's descent results (its own id and -1 entries are ignored).  Rescued
+ * (displaced) neighbours go to d_resc_ids / d_resc_dists (node_count, k_nn),
+ * -1 padded, in their former slot order.  d_changed (optional) counts the rows
+ * whose direct set changed. */
+int ggnn_merge_rows(int64_t node_count, int32_t k, int32_t k_nn, int32_t *d_adj, double *d_nnd, int32_t *d_sym_count,
+                    double *d_dnn1, const int32_t *d_hit_ids, const double *d_hit_dists, int32_t hits_per_node,
+                    int32_t *d_resc_ids, double *d_resc_dists, int32_t *d_changed, void *stream);
+
+/* Replaces: the check half of symmetrize (build.py:200-266 with
+ * sym_check_pair, _core.pyx:375-435) for every (x, z) of a layer: pair
+ * p = x * per_node + t checks direct slot t < k_nn of x, or rescued entry
+ * t - k_nn (d_resc_ids (node_count, per_node - k_nn), may be NULL).  Pairs
+ * with verdict 2 are appended to d_req as {p, x, z, fallback[n_fallback]}
+ * (int32, stride 3 + n_fallback); *d_req_count counts them (it may exceed
+ * req_cap, in which case the surplus was not stored). */
+int ggnn_sym_check_layer(const ggnn_vectors *X, const ggnn_layer *layer, const double *d_nnd,
+                         const int32_t *d_resc_id, const double *d_resc_d, int32_t per_node, double tau,
+                         double d_nn1_max, int32_t budget, int32_t k_out, int32_t prioq_size, int32_t visited_size,
+                         int32_t n_fallback, int32_t *d_req, int32_t *d_req_count, int64_t req_cap, void *stream);
+
+/* Replaces: the claim half of symmetrize (reserve_sym_slot, graph.py:167-191,
+ * and the fallback loop of build.py:237-244).  Each destination accepts the
+ * requests in ascending pair-index order while it has room and does not yet
+ * hold x; rejected requests move to their next fallback.  d_best_scratch is
+ * a node_count int32 array that must hold INT32_MAX (it is left that way);
+ * stage / tgt scratch hold req_cap int32.  *d_dropped += requests with no taker. */
+int ggnn_sym_claim(const int32_t *d_req, const int32_t *d_req_count, int64_t req_cap, int32_t n_fallback,
+                   int32_t *d_adj, int32_t *d_sym_count, int32_t k, int32_t k_nn, int32_t *d_best_scratch,
+                   int32_t *d_stage_scratch, int32_t *d_tgt_scratch, int32_t *d_dropped, void *stream);
+
+/* Replaces: compute_stats (build.py:275-280) / live_d_nn1_max
+ * (graph.py:196-199): d_out[4] = {max of finite values (0 if none), sum of
+ * finite values, count of finite values, count of non-finite values}. */
+int ggnn_layer_stats(const double *d_values, int64_t n, double *d_scratch, double *d_out, void *stream);
+size_t ggnn_layer_stats_scratch_bytes(void);
+
 #ifdef __cplusplus
 }
 #endif

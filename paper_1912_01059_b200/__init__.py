@@ -22,6 +22,17 @@ from .search import (
     stopping_check,
     top_layer_seeds,
 )
-from .build import plan_geometry, partition_bottom, select_points
+from .build import (
+    BuildStats,
+    build,
+    build_base,
+    compute_stats,
+    merge_layer,
+    partition_bottom,
+    plan_geometry,
+    refine_layer,
+    select_points,
+    symmetrize,
+)
 
 __version__ = "0.1.0"

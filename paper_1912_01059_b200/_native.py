@@ -65,8 +65,15 @@ _SIGS = {
     "ggnn_squared_l2_many": [P, P, P, I32, P, P],
     "ggnn_f32_to_u8": [P, I64, P, P, P],
     "ggnn_leaf_knn": [P, P, P, P, I64, I64, I32, P, P, P, I32, P, P, P, P],
+    "ggnn_merge_descent": [P, P, I32, I32, I32, P, I64, P, I32, I32, P, P, P, P, P],
+    "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
+    "ggnn_sym_check_layer": [P, P, P, P, P, I32, F64, F64, I32, I32, I32, I32, I32, P, P, I64, P],
+    "ggnn_sym_claim": [P, P, I64, I32, P, P, I32, I32, P, P, P, P, P],
+    "ggnn_layer_stats": [P, I64, P, P, P],
+    "ggnn_layer_stats_scratch_bytes": [],
 }
-_RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t}
+_RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t,
+             "ggnn_layer_stats_scratch_bytes": ctypes.c_size_t}
 # entry points added by later translation units register themselves here
 EXTRA_SIGS: dict = {}
 
@@ -135,9 +142,13 @@ def ptr(t) -> P:
 
 
 def to_dev(a: np.ndarray, dtype=None):
+    import warnings
+
     t = torch()
     arr = np.ascontiguousarray(a if dtype is None else a.astype(dtype, copy=False))
-    return t.from_numpy(arr).to(device(), non_blocking=False)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)  # read-only arrays are only read
+        return t.from_numpy(arr).to(device(), non_blocking=False)
 
 
 def empty(shape, dtype):

@@ -131,6 +131,231 @@ __global__ void __launch_bounds__(256) leaf_knn_kernel(const __grid_constant__ L
   }
 }
 
+// ------------------------------------------------------------- merge rows
+// One warp per node x: direct slots := the k_nn smallest (dist, id) of the
+// current direct list united with the descent hits (x itself and ids already
+// direct excluded); ids that become direct leave the inverse slots (order of
+// the rest kept); displaced former neighbours go to the rescued list in their
+// former order -- AdjacencyLayer.merge_hits (graph.py:121-165).
+struct MergeArgs {
+  int64_t nc;
+  int k, k_nn;
+  int32_t* adj;
+  double* nnd;
+  int32_t* symc;
+  double* dnn1;
+  const int32_t* hit_id;  // (nc, nh)
+  const double* hit_d;
+  int nh;
+  int32_t* resc_id;       // (nc, k_nn), -1 padded
+  double* resc_d;
+  int32_t* changed;       // count of rows whose direct set changed (optional)
+};
+
+__global__ void __launch_bounds__(256) merge_rows_kernel(const __grid_constant__ MergeArgs a) {
+  const int64_t x = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (x >= a.nc) return;
+  const int lane = lane_id();
+  const int k_nn = a.k_nn, k = a.k;
+  int32_t* row = a.adj + x * k;
+  int cid = lane < k_nn ? row[lane] : -1;
+  double cd = lane < k_nn ? a.nnd[x * k_nn + lane] : 0.0;
+  const int ncur = __popc(__ballot_sync(FULL, lane < k_nn && cid >= 0));  // direct slots are a prefix
+  if (lane >= ncur) cid = -1;
+  int hid = lane < a.nh ? a.hit_id[x * a.nh + lane] : -1;
+  double hd = lane < a.nh ? a.hit_d[x * a.nh + lane] : 0.0;
+  bool hv = hid >= 0 && hid != (int)x;
+  for (int i = 0; i < ncur; ++i) hv = hv && hid != __shfl_sync(FULL, cid, i);
+  const int nextra = __popc(__ballot_sync(FULL, hv));
+  int32_t* rid = a.resc_id + x * k_nn;
+  if (nextra == 0) {
+    if (lane < k_nn) rid[lane] = -1;
+    return;
+  }
+  double bk = lane < ncur ? cd : KeyOps<double>::max_key();
+  int bi = lane < ncur ? cid : INT_MAX;
+  topk_merge_chunk(bk, bi, hv ? hd : KeyOps<double>::max_key(), hv ? hid : INT_MAX, k_nn);
+  const int nnew = __popc(__ballot_sync(FULL, lane < k_nn && bi != INT_MAX));
+  bool in_new = false;
+  for (int j = 0; j < nnew; ++j) in_new = in_new || (cid >= 0 && cid == __shfl_sync(FULL, bi, j));
+  const bool evicted = lane < ncur && !in_new;
+  const unsigned em = __ballot_sync(FULL, evicted);
+  if (em == 0u && nnew == ncur) {  // same set: nothing changes
+    if (lane < k_nn) rid[lane] = -1;
+    return;
+  }
+  const int erank = __popc(em & lanemask_lt());
+  if (lane < k_nn) rid[lane] = -1;
+  __syncwarp();
+  if (evicted) {
+    rid[erank] = cid;
+    a.resc_d[x * k_nn + erank] = cd;
+  }
+  // inverse slots: drop ids that became direct, keep the order of the rest
+  const int ns = a.symc[x];
+  int sid = lane < ns ? row[k_nn + lane] : -1;
+  bool keep = lane < ns;
+  for (int j = 0; j < nnew; ++j) keep = keep && sid != __shfl_sync(FULL, bi, j);
+  const unsigned km = __ballot_sync(FULL, keep);
+  const int nkeep = __popc(km);
+  __syncwarp();
+  if (lane < k - k_nn) row[k_nn + lane] = -1;
+  __syncwarp();
+  if (keep) row[k_nn + __popc(km & lanemask_lt())] = sid;
+  if (lane < k_nn) {
+    row[lane] = lane < nnew ? bi : -1;
+    a.nnd[x * k_nn + lane] = lane < nnew ? bk : KeyOps<double>::max_key();
+  }
+  if (lane == 0) {
+    a.symc[x] = nkeep;
+    a.dnn1[x] = bk;
+    if (a.changed) atomicAdd(a.changed, 1);
+  }
+}
+
+// --------------------------------------------------------- inverse claims
+// Deterministic resolution of the verdict-2 requests of one symmetrize pass.
+// Request r = {pair index p, x, z, fallbacks}.  Every round each open request
+// proposes to its current target (z, then the fallbacks in order), skipping
+// targets that are full or already hold x; each target accepts the proposal
+// with the smallest pair index, so claims land in the reference's (x, slot)
+// priority order per destination (reserve_sym_slot, graph.py:167-191).
+// Requests with no taker are dropped.  A single CTA suffices: requests are a
+// small fraction (~0.3%) of the checked pairs.
+struct ClaimArgs {
+  const int32_t* req;
+  const int32_t* req_count;
+  int64_t req_cap;
+  int n_fallback;
+  int32_t* adj;
+  int32_t* symc;
+  int k, k_nn;
+  int32_t* best;   // (node_count) scratch, INT_MAX on entry and on exit
+  int32_t* stage;  // (req_cap) scratch
+  int32_t* tgt;    // (req_cap) scratch
+  int32_t* dropped;
+};
+
+__global__ void __launch_bounds__(1024) sym_claim_kernel(const __grid_constant__ ClaimArgs a) {
+  const int64_t nreq = min((int64_t)*a.req_count, a.req_cap);
+  const int stride = 3 + a.n_fallback;
+  const int k_sym = a.k - a.k_nn;
+  __shared__ int active;
+  for (int64_t r = threadIdx.x; r < nreq; r += blockDim.x) {
+    a.stage[r] = 0;
+    a.tgt[r] = -1;
+  }
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) active = 0;
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < nreq; r += blockDim.x) {
+      int s = a.stage[r];
+      if (s < 0) continue;
+      const int32_t* q = a.req + r * stride;
+      const int x = q[1];
+      for (;;) {
+        const int t = s == 0 ? q[2] : (s <= a.n_fallback ? q[2 + s] : -1);
+        if (t < 0) {
+          s = -2;
+          atomicAdd(a.dropped, 1);
+          break;
+        }
+        if (t != x) {
+          const int used = a.symc[t];
+          bool ok = used < k_sym;
+          const int32_t* trow = a.adj + (int64_t)t * a.k;
+          for (int j = 0; ok && j < a.k_nn + used; ++j) ok = trow[j] != x;
+          if (ok) {
+            atomicMin(a.best + t, q[0]);
+            a.tgt[r] = t;
+            active = 1;
+            break;
+          }
+        }
+        ++s;
+      }
+      a.stage[r] = s;
+    }
+    __syncthreads();
+    if (!active) break;
+    for (int64_t r = threadIdx.x; r < nreq; r += blockDim.x) {
+      const int t = a.tgt[r];
+      if (t < 0) continue;
+      const int32_t* q = a.req + r * stride;
+      if (a.best[t] == q[0]) {
+        const int used = a.symc[t];
+        a.adj[(int64_t)t * a.k + a.k_nn + used] = q[1];
+        a.symc[t] = used + 1;
+        a.stage[r] = -1;
+      }
+    }
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < nreq; r += blockDim.x) {
+      const int t = a.tgt[r];
+      if (t >= 0) {
+        a.best[t] = INT_MAX;
+        a.tgt[r] = -1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ layer stats
+// out[0] = max over finite d_nn1 (0 if none), out[1] = sum, out[2] = count of
+// finite values, out[3] = count of non-finite values.  Two passes with a
+// fixed grid, so the sum order (and the mean) is deterministic.
+constexpr int STATS_BLOCKS = 296;
+
+__global__ void __launch_bounds__(256) stats_partial_kernel(const double* v, int64_t n, double* part) {
+  double mx = 0.0, sum = 0.0, cnt = 0.0, bad = 0.0;
+  bool any = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double x = v[i];
+    if (isfinite(x)) {
+      mx = any ? fmax(mx, x) : x;
+      any = true;
+      sum += x;
+      cnt += 1.0;
+    } else {
+      bad += 1.0;
+    }
+  }
+  __shared__ double sm[4][256];
+  sm[0][threadIdx.x] = any ? mx : -1.0;
+  sm[1][threadIdx.x] = sum;
+  sm[2][threadIdx.x] = cnt;
+  sm[3][threadIdx.x] = bad;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sm[0][threadIdx.x] = fmax(sm[0][threadIdx.x], sm[0][threadIdx.x + o]);
+      sm[1][threadIdx.x] += sm[1][threadIdx.x + o];
+      sm[2][threadIdx.x] += sm[2][threadIdx.x + o];
+      sm[3][threadIdx.x] += sm[3][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 4; ++c) part[blockIdx.x * 4 + c] = sm[c][0];
+}
+
+__global__ void stats_final_kernel(const double* part, int nparts, double* out) {
+  if (threadIdx.x != 0) return;
+  double mx = -1.0, sum = 0.0, cnt = 0.0, bad = 0.0;
+  for (int i = 0; i < nparts; ++i) {
+    mx = fmax(mx, part[i * 4]);
+    sum += part[i * 4 + 1];
+    cnt += part[i * 4 + 2];
+    bad += part[i * 4 + 3];
+  }
+  out[0] = mx < 0.0 ? 0.0 : mx;
+  out[1] = sum;
+  out[2] = cnt;
+  out[3] = bad;
+}
+
 }  // namespace ggnn
 
 using namespace ggnn;
@@ -177,5 +402,43 @@ int ggnn_leaf_knn(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* 
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
+
+int ggnn_merge_rows(int64_t node_count, int32_t k, int32_t k_nn, int32_t* d_adj, double* d_nnd, int32_t* d_sym_count,
+                    double* d_dnn1, const int32_t* d_hit_ids, const double* d_hit_dists, int32_t hits_per_node,
+                    int32_t* d_resc_ids, double* d_resc_dists, int32_t* d_changed, void* stream) {
+  GGNN_CHECK_ARG(d_adj && d_nnd && d_sym_count && d_dnn1 && d_hit_ids && d_hit_dists && d_resc_ids && d_resc_dists,
+                 "invalid arguments");
+  GGNN_CHECK_ARG(k >= 1 && k <= MAX_K && k_nn >= 1 && k_nn <= k && hits_per_node >= 0 && hits_per_node <= 32,
+                 "invalid merge geometry");
+  if (node_count <= 0) return GGNN_OK;
+  MergeArgs a{node_count, k, k_nn, d_adj, d_nnd, d_sym_count, d_dnn1, d_hit_ids, d_hit_dists, hits_per_node,
+              d_resc_ids, d_resc_dists, d_changed};
+  merge_rows_kernel<<<(unsigned)((node_count + 7) / 8), 256, 0, as_stream(stream)>>>(a);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_sym_claim(const int32_t* d_req, const int32_t* d_req_count, int64_t req_cap, int32_t n_fallback,
+                   int32_t* d_adj, int32_t* d_sym_count, int32_t k, int32_t k_nn, int32_t* d_best_scratch,
+                   int32_t* d_stage_scratch, int32_t* d_tgt_scratch, int32_t* d_dropped, void* stream) {
+  GGNN_CHECK_ARG(d_req && d_req_count && d_adj && d_sym_count && d_best_scratch && d_stage_scratch && d_tgt_scratch &&
+                 d_dropped, "invalid arguments");
+  ClaimArgs a{d_req, d_req_count, req_cap, n_fallback, d_adj, d_sym_count, k, k_nn, d_best_scratch, d_stage_scratch,
+              d_tgt_scratch, d_dropped};
+  sym_claim_kernel<<<1, 1024, 0, as_stream(stream)>>>(a);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_layer_stats(const double* d_values, int64_t n, double* d_scratch, double* d_out, void* stream) {
+  GGNN_CHECK_ARG(d_values && d_scratch && d_out && n >= 0, "invalid arguments");
+  cudaStream_t st = as_stream(stream);
+  stats_partial_kernel<<<STATS_BLOCKS, 256, 0, st>>>(d_values, n, d_scratch);
+  stats_final_kernel<<<1, 32, 0, st>>>(d_scratch, STATS_BLOCKS, d_out);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+size_t ggnn_layer_stats_scratch_bytes(void) { return (size_t)STATS_BLOCKS * 4 * sizeof(double); }
 
 }  // extern "C"

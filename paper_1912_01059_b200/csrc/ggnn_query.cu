@@ -10,6 +10,7 @@
 #include <mutex>
 #include <string>
 
+#include "ggnn_build.h"
 #include "ggnn_capi_util.cuh"
 #include "ggnn_search.cuh"
 
@@ -700,6 +701,81 @@ int ggnn_descent_batch(const ggnn_vectors* X, const ggnn_layer* layers, int32_t 
     case 1: return launch_warps(descent_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
     default: return launch_warps(descent_kernel<uint8_t, float>, a, a.m, a.region, st);
   }
+}
+
+int ggnn_merge_descent(const ggnn_vectors* X, const ggnn_layer* layers, int32_t num_layers, int32_t start,
+                       int32_t stop, const int32_t* d_query_rows, int64_t m, const int32_t* d_seg_of, int32_t seg_div,
+                       int32_t seg_size, const ggnn_search_params* p, int32_t* d_ids, double* d_dists,
+                       int32_t* d_counters, void* stream) {
+  GGNN_CHECK_ARG(d_query_rows && seg_div >= 1 && seg_size >= 1, "invalid merge descent arguments");
+  ggnn_queries q{nullptr, d_query_rows, m, X ? X->dtype : 0, 0};
+  SearchArgs a;
+  int rc = fill_common(a, X, &q, p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(layers && num_layers >= 1 && num_layers <= MAX_LAYERS, "1..%d layers supported", MAX_LAYERS);
+  GGNN_CHECK_ARG(0 <= stop && stop <= start && start < num_layers, "invalid layer range");
+  for (int j = 0; j < num_layers; ++j) {
+    GGNN_CHECK_ARG(layers[j].k >= 1 && layers[j].k <= MAX_K, "invalid layer %d", j);
+    if (j > stop && j <= start) GGNN_CHECK_ARG(layers[j].d_down != nullptr, "layer %d needs a down map", j);
+    a.layers[j] = to_dev(layers[j]);
+  }
+  a.start = start;
+  a.stop = stop;
+  a.seg_of = d_seg_of;
+  a.seg_div = seg_div;
+  a.seg_size = seg_size;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  a.counters = d_counters;
+  cudaStream_t st = as_stream(stream);
+  if (X->dtype == GGNN_F32) return launch_warps(descent_kernel<float, float>, a, a.m, a.region, st);
+  return launch_warps(descent_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
+}
+
+int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const double* d_nnd,
+                         const int32_t* d_resc_id, const double* d_resc_d, int32_t per_node, double tau,
+                         double d_nn1_max, int32_t budget, int32_t k_out, int32_t prioq_size, int32_t visited_size,
+                         int32_t n_fallback, int32_t* d_req, int32_t* d_req_count, int64_t req_cap, void* stream) {
+  GGNN_CHECK_ARG(X && X->d_data && layer && layer->d_adj && d_nnd && d_req && d_req_count, "invalid arguments");
+  GGNN_CHECK_ARG(layer->k >= 1 && layer->k <= MAX_K && per_node >= layer->k_nn, "invalid layer geometry");
+  GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32 && n_fallback >= 0 && n_fallback <= 32, "k_out / n_fallback in [1, 32]");
+  int64_t npairs = layer->node_count * per_node;
+  if (npairs <= 0) return GGNN_OK;
+  SymArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = X->d_data;
+  a.d = X->d;
+  a.lpr = choose_lpr(X->d, X->dtype, X->dtype, reinterpret_cast<uintptr_t>(X->d_data));
+  a.layer = to_dev(*layer);
+  a.npairs = npairs;
+  ggnn_search_params p{k_out, prioq_size, visited_size, 0, tau, budget};
+  a.c = make_cfg(&p);
+  a.dmax = d_nn1_max;
+  a.n_fallback = n_fallback;
+  a.nnd = d_nnd;
+  a.k_nn = layer->k_nn;
+  a.resc_id = d_resc_id;
+  a.resc_d = d_resc_d;
+  a.per_node = per_node;
+  a.req = d_req;
+  a.req_count = d_req_count;
+  a.req_cap = req_cap;
+  int keysize = X->dtype == GGNN_U8 ? 4 : 8;
+  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
+  int W = pick_warps(a.region, 8);
+  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
+  size_t smem = (size_t)W * a.region;
+  cudaStream_t st = as_stream(stream);
+  int64_t grid = (npairs + W - 1) / W;
+  if (X->dtype == GGNN_U8) {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);
+  } else {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    symcheck_kernel<float><<<(unsigned)grid, W * 32, smem, st>>>(a);
+  }
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
 }
 
 int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const int32_t* d_x, const int32_t* d_z,

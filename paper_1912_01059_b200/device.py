@@ -172,6 +172,11 @@ def device_hierarchy(h) -> DeviceHierarchy:
     cache = h._device_cache
     if cache is not None and cache[0] == tok:
         return cache[1]
-    dh = DeviceHierarchy(h)
+    if all(L.device_authoritative and "rows_q" in L._dev for L in h.layers):
+        from ._devgraph import device_hierarchy_from_build
+
+        dh = device_hierarchy_from_build(h)  # layers already in searchable device form
+    else:
+        dh = DeviceHierarchy(h)
     h._device_cache = (tok, dh)
     return dh

@@ -224,3 +224,18 @@ def descent_arrays(h, queries, cfg: QueryConfig, start: int, stop: int, seg_lo=N
            N.stream_ptr())
     del keep
     return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())
+
+
+def exact_knn_rows(dataset, rows: np.ndarray, k: int):
+    """Exact top-k (k <= 32) of dataset rows `rows` against the whole dataset,
+    ties by ascending id, in one launch of ggnn_exhaustive_topk."""
+    dv = DeviceVectors.of(dataset)
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    t = N.torch()
+    rd = N.to_dev(rows)
+    qs = N.queries_struct(rows=rd, dtype_code=dv.dtype)
+    ids = N.empty((len(rows), k), t.int32)
+    dists = N.empty((len(rows), k), t.float64)
+    N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), N.ptr(ids),
+           N.ptr(dists), N.stream_ptr())
+    return ids.cpu().numpy(), dists.cpu().numpy()
