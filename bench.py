@@ -1,0 +1,440 @@
+"""GGNN B200 benchmark: QPS at R@10 >= 0.99 on SIFT1M-shaped data + build seconds.
+
+Workload (BASELINE.json configs[1], "C2"): synthetic SIFT1M-shaped latent16
+data (SURVEY.md 8d "G_B"), 1M x 128 integer-valued (stored losslessly as
+uint8 on the device), 10k queries, k=10, BuildConfig(seed=7) defaults
+(k=24, k_nn=12, s=32, g=4, refinements=2, tau_build=0.5).  tau is chosen in
+the run: the smallest tau of a sweep whose R@10 (reference `recall_at`,
+evaluate.py:60-76) against exact ground truth computed on the GPU in the same
+run is >= 0.99.
+
+A "step" is one batch of 10k queries through the query kernel with inputs
+resident in HBM.  Multi-GPU: one process per GPU, every rank holds the full
+1M index and answers its own 10k-query batch (queries are independent units;
+no data-path collective), so `scaling` is "weak".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ggnn|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "queries/sec at R@10>=0.99 (SIFT1M-shape, k=10); index build seconds"
+UNIT = "queries/s"
+TAUS = [0.2, 0.25, 0.3, 0.35, 0.4, 0.45, 0.5, 0.55, 0.6, 0.7, 0.8]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ggnn", choices=["ggnn", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--queries", type=int, default=10_000)
+    ap.add_argument("--tau", type=float, default=None, help="skip the sweep and use this tau")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ dist
+class Dist:
+    def __init__(self, torch, n_gpus):
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.on = self.world > 1
+        if self.on:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+
+    def barrier(self):
+        if self.on:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.on:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.on:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ data
+def make_workload(args):
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, queries = make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234)
+    return base, queries
+
+
+def recall_at(ids, gt_first, k):
+    return float(np.mean((ids[:, :k] == gt_first[:, None]).any(axis=1)))
+
+
+def k_recall_at(ids, gt, k):
+    return float(np.mean([len(set(ids[i, :k].tolist()) & set(gt[i, :k].tolist())) / k for i in range(len(ids))]))
+
+
+def choose_tau(ga, h, Q, gt_ids, fixed):
+    sweep = []
+    taus = [fixed] if fixed is not None else TAUS
+    chosen = None
+    for tau in taus:
+        res = ga.query_arrays(h, Q, ga.QueryConfig(k_out=10, tau=tau))
+        row = {"tau": tau, "R@1": recall_at(res.ids, gt_ids[:, 0], 1), "R@10": recall_at(res.ids, gt_ids[:, 0], 10),
+               "kR@10": k_recall_at(res.ids, gt_ids, 10), "V": float(res.counters[:, 0].mean()),
+               "T": float(res.counters[:, 1].mean())}
+        sweep.append(row)
+        if chosen is None and row["R@10"] >= 0.99:
+            chosen = row
+            if fixed is None:
+                break
+    if chosen is None:
+        chosen = sweep[-1]
+    return chosen, sweep
+
+
+# --------------------------------------------------------- CPU baseline
+def export_graph(h, base, Q, tau):
+    """Dump the GPU-built graph + workload as .npy files (shared, memory-mapped
+    by every CPU worker) -- the same arrays GGNN v1 persists."""
+    import tempfile
+
+    root = Path(tempfile.mkdtemp(prefix="ggnn_cpu_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None))
+    np.save(root / "base.npy", np.ascontiguousarray(base, dtype=np.float32))
+    np.save(root / "queries.npy", np.ascontiguousarray(Q, dtype=np.float32))
+    for j, L in enumerate(h.layers):
+        np.save(root / f"adj{j}.npy", L.adjacency)
+        np.save(root / f"nnd{j}.npy", L.nn_dists)
+        np.save(root / f"sym{j}.npy", L.sym_count)
+        np.save(root / f"dnn1_{j}.npy", L.d_nn1)
+        if j:
+            np.save(root / f"tob{j}.npy", h.to_bottom[j])
+    c = h.config
+    meta = {"layers": h.num_layers, "s": h.s, "g": h.g, "k": c.k, "k_nn": c.k_nn, "k_sym": c.k_sym,
+            "refinements": c.refinements, "tau_build": c.tau_build, "seed": c.seed,
+            "stats": [h.stats.d_nn1_mean, h.stats.d_nn1_max], "tau": tau}
+    (root / "meta.json").write_text(json.dumps(meta))
+    return root
+
+
+def _load_ref_hierarchy(root: Path):
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    import graphann_ref as R  # noqa: E402
+
+    meta = json.loads((root / "meta.json").read_text())
+    cfg = R.BuildConfig(k=meta["k"], k_nn=meta["k_nn"], k_sym=meta["k_sym"], s=meta["s"], g=meta["g"],
+                        refinements=meta["refinements"], tau_build=meta["tau_build"], seed=meta["seed"])
+    layers, tob = [], [None]
+    for j in range(meta["layers"]):
+        adj = np.load(root / f"adj{j}.npy", mmap_mode="r")
+        L = R.AdjacencyLayer.__new__(R.AdjacencyLayer)
+        L.node_count, L.k, L.k_nn = adj.shape[0], meta["k"], meta["k_nn"]
+        L.k_sym = L.k - L.k_nn
+        L.adjacency = adj
+        L.nn_dists = np.load(root / f"nnd{j}.npy", mmap_mode="r")
+        L.sym_count = np.load(root / f"sym{j}.npy", mmap_mode="r")
+        L.d_nn1 = np.load(root / f"dnn1_{j}.npy", mmap_mode="r")
+        layers.append(L)
+        if j:
+            tob.append(np.load(root / f"tob{j}.npy"))
+    h = R.Hierarchy(layers, tob, meta["s"], meta["g"], cfg, R.GraphStats(*meta["stats"]),
+                    dim=int(np.load(root / "base.npy", mmap_mode="r").shape[1]))
+    h.attach(R.Dataset(np.load(root / "base.npy", mmap_mode="r")))
+    return R, h, meta
+
+
+def _ref_worker(job):
+    """Child process: the reference's own batch_query on a query slice."""
+    root, lo, hi = job
+    R, h, meta = _load_ref_hierarchy(Path(root))
+    Q = np.load(Path(root) / "queries.npy", mmap_mode="r")[lo:hi]
+    t0 = time.perf_counter()
+    res = R.batch_query(h, np.ascontiguousarray(Q), R.QueryConfig(k_out=10, tau=meta["tau"]), threads=1)
+    dt = time.perf_counter() - t0
+    ids = np.stack([np.pad(r.ids, (0, 10 - len(r.ids)), constant_values=-1) for r in res])
+    return dt, ids
+
+
+def cpu_reference_qps(root: Path, nq_total: int, target_seconds: float, max_procs=None):
+    """Process-parallel reference batch_query (threads do not scale under the
+    GIL): one process per host core on a bounded query sample."""
+    import multiprocessing as mp
+
+    cores = max_procs or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    probe = min(20, nq_total)
+    with ctx.Pool(1) as pool:
+        dt, _ = pool.map(_ref_worker, [(str(root), 0, probe)])[0]
+    per_q = dt / probe
+    per_proc = max(1, int(target_seconds / max(per_q, 1e-6)))
+    per_proc = min(per_proc, max(1, nq_total // cores))
+    jobs = [(str(root), i * per_proc, (i + 1) * per_proc) for i in range(cores) if (i + 1) * per_proc <= nq_total]
+    with ctx.Pool(len(jobs)) as pool:
+        out = pool.map(_ref_worker, jobs)
+    inner = max(o[0] for o in out)
+    nq = sum(j[2] - j[1] for j in jobs)
+    ids = np.concatenate([o[1] for o in out])
+    tau = json.loads((root / "meta.json").read_text())["tau"]
+    return {"value": nq / inner, "unit": UNIT, "cores": len(jobs), "kind": "reference",
+            "sample": f"{nq} queries ({len(jobs)} processes x {per_proc}) of the same workload on the GPU-built "
+                      f"graph, reference graphann.batch_query (compiled _core), tau={tau}",
+            "ids": ids, "n": nq}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    import torch
+
+    dist = Dist(torch, args.gpus)
+    import paper_1912_01059_b200 as ga
+    from paper_1912_01059_b200 import _native as N
+
+    if args.impl == "reference":
+        return run_reference(args, dist, ga)
+
+    base, Q = make_workload(args)
+    ds = ga.Dataset(base)
+    cfg = ga.BuildConfig(seed=7)
+    dist.barrier()
+    h, bstats = ga.build(ds, cfg)
+    build_s = dist.max(bstats.build_seconds)
+
+    gt_ids, _ = ga.search.exact_knn(ds, Q, 10)
+    chosen, sweep = choose_tau(ga, h, Q, gt_ids, args.tau)
+    tau = chosen["tau"]
+    qcfg = ga.QueryConfig(k_out=10, tau=tau)
+
+    # ---- device-resident kernel timing (value) ------------------------
+    from paper_1912_01059_b200.device import device_hierarchy
+
+    dh = device_hierarchy(h)
+    dv = dh.vectors
+    dq, qs = dv.queries(Q)
+    m = Q.shape[0]
+    ids = N.empty((m, 10), torch.int32)
+    dists = N.empty((m, 10), torch.float64)
+    cnt = N.empty((m, 5), torch.int32)
+    params = N.search_params(10, qcfg.prioq_size, qcfg.visited_size, tau, qcfg.max_iterations, 0)
+
+    def step():
+        N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
+               N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, N.ptr(ids),
+               N.ptr(dists), N.ptr(cnt), None, 0, N.stream_ptr())
+
+    for _ in range(args.warmup):
+        step()
+    stream = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        evs[0].record(stream)
+        for i in range(args.steps):
+            step()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    t_total = evs[0].elapsed_time(evs[-1]) / 1e3
+    t_max = dist.max(t_total)
+    per_launch = [evs[i].elapsed_time(evs[i + 1]) / 1e3 for i in range(args.steps)]
+    value = args.gpus * m * args.steps / t_max
+    c = cnt.cpu().numpy().astype(np.int64)
+    e = 1 if dv.exact_integers else 4
+    d = base.shape[1]
+    kk = dh.layers[0].k
+    bytes_per_launch = int((c[:, 0] * d * e + c[:, 1] * (4 * kk + 4) + d * e + 8 * 10).sum())
+    avg_launch = float(np.mean(per_launch))
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_per_launch / avg_launch / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "query_kernel_ncu.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    # ---- end to end through the public API (host buffers) --------------
+    Q_host = np.ascontiguousarray(Q, dtype=np.float32)
+    for _ in range(max(1, args.warmup)):
+        ga.query_arrays(h, Q_host, qcfg)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = ga.query_arrays(h, Q_host, qcfg)
+    torch.cuda.synchronize()
+    e2e_t = dist.max(time.perf_counter() - t0)
+    e2e = {"value": args.gpus * m * args.steps / e2e_t, "unit": UNIT,
+           "h2d_bytes_per_step": int(m * d * (1 if dv.exact_integers else 4)),
+           "d2h_bytes_per_step": int(out.ids.nbytes + out.dists.nbytes + out.counters.nbytes),
+           "api": "paper_1912_01059_b200.query_arrays(h, numpy queries) -> host arrays"}
+
+    # ---- CPU baseline (rank 0, N == 1) ---------------------------------
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        if (ROOT / "oracle" / "_ref" / "graphann_ref").exists():
+            import shutil
+
+            root = export_graph(h, base, Q, tau)
+            try:
+                cpu = cpu_reference_qps(root, m, args.cpu_seconds)
+            finally:
+                shutil.rmtree(root, ignore_errors=True)
+            ref_ids = cpu.pop("ids")
+            cpu["ids_equal_to_gpu"] = float(np.mean(np.all(ref_ids == out.ids[: cpu.pop("n")], axis=1)))
+        else:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": "oracle/_ref not built on this box"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8" if dv.exact_integers else "f32",
+        "data": "synthetic latent16 (SURVEY.md 8d G_B), seed 1234",
+        "config": {"workload": f"SIFT1M-shaped latent16 {args.n}x{args.d}, {m} queries/rank, k=10, k_build=24",
+                   "tau": tau, "recall": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
+                   "mean_visited": chosen["V"], "mean_steps": chosen["T"], "tau_sweep": sweep,
+                   "build_seconds": build_s, "build_phase_seconds_top": dict(sorted(
+                       bstats.phase_seconds.items(), key=lambda kv: -kv[1])[:6]),
+                   "parallelism": f"replicas x{args.gpus} (independent query batches)",
+                   "l2": "inputs larger than L2 (u8 vectors 128 MB + adjacency 96 MB)"},
+        "build_seconds": build_s,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "kernel_ms": avg_launch * 1e3, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"},
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    if dist.rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            Path(args.out).write_text(s + "\n")
+    dist.close()
+
+
+def run_reference(args, dist, ga):
+    """--impl reference: the reference's own CPU query path (graphann
+    batch_query, compiled _core) on this box's host cores, process-parallel,
+    on a bounded sample of the same workload per step."""
+    if dist.rank != 0:
+        dist.close()
+        return
+    base, Q = make_workload(args)
+    ds = ga.Dataset(base)
+    h, bstats = ga.build(ds, ga.BuildConfig(seed=7))  # index prep (untimed): the GPU-built graph
+    gt_ids, _ = ga.search.exact_knn(ds, Q, 10)
+    chosen, sweep = choose_tau(ga, h, Q, gt_ids, args.tau)
+    tau = chosen["tau"]
+    if not (ROOT / "oracle" / "_ref" / "graphann_ref").exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (compiled reference) not present"}))
+        return
+    import shutil
+
+    root = export_graph(h, base, Q, tau)
+    per_step = max(5.0, min(args.cpu_seconds, 240.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    info = None
+    try:
+        for i in range(args.warmup + args.steps):
+            r = cpu_reference_qps(root, Q.shape[0], per_step)
+            r.pop("ids")
+            r.pop("n")
+            if i >= args.warmup:
+                vals.append(r["value"])
+                info = r
+    finally:
+        shutil.rmtree(root, ignore_errors=True)
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic latent16 (SURVEY.md 8d G_B)",
+        "config": {"workload": f"SIFT1M-shaped latent16 {args.n}x{args.d}, k=10, k_build=24", "tau": tau,
+                   "recall_gpu_same_tau": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")}},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -52,8 +52,8 @@ int ggnn_merge_rows(int64_t node_count, int32_t k, int32_t k_nn, int32_t *d_adj,
  * sym_check_pair, _core.pyx:375-435) for every (x, z) of a layer: pair
  * p = x * per_node + t checks direct slot t < k_nn of x, or rescued entry
  * t - k_nn (d_resc_ids (node_count, per_node - k_nn), may be NULL).  Pairs
- * with verdict 2 are appended to d_req as {p, x, z, fallback[n_fallback]}
- * (int32, stride 3 + n_fallback); *d_req_count counts them (it may exceed
+ * with verdict 2 are appended to d_req as {p, x, z, d_xz lo, d_xz hi,
+ * fallback[n_fallback]} (int32, stride 5 + n_fallback); *d_req_count counts them (it may exceed
  * req_cap, in which case the surplus was not stored). */
 int ggnn_sym_check_layer(const ggnn_vectors *X, const ggnn_layer *layer, const double *d_nnd,
                          const int32_t *d_resc_id, const double *d_resc_d, int32_t per_node, double tau,
@@ -61,14 +61,32 @@ int ggnn_sym_check_layer(const ggnn_vectors *X, const ggnn_layer *layer, const d
                          int32_t n_fallback, int32_t *d_req, int32_t *d_req_count, int64_t req_cap, void *stream);
 
 /* Replaces: the claim half of symmetrize (reserve_sym_slot, graph.py:167-191,
- * and the fallback loop of build.py:237-244).  Each destination accepts the
- * requests in ascending pair-index order while it has room and does not yet
- * hold x; rejected requests move to their next fallback.  d_best_scratch is
- * a node_count int32 array that must hold INT32_MAX (it is left that way);
- * stage / tgt scratch hold req_cap int32.  *d_dropped += requests with no taker. */
-int ggnn_sym_claim(const int32_t *d_req, const int32_t *d_req_count, int64_t req_cap, int32_t n_fallback,
-                   int32_t *d_adj, int32_t *d_sym_count, int32_t k, int32_t k_nn, int32_t *d_best_scratch,
-                   int32_t *d_stage_scratch, int32_t *d_tgt_scratch, int32_t *d_dropped, void *stream);
+ * and the fallback loop of build.py:237-244) -- one round.  Requests are the
+ * records written by ggnn_sym_check_layer ({p, x, z, d_xz lo, d_xz hi,
+ * fallback[n_fallback]}); d_stage[r] >= 0 is the index of the request's
+ * current target (0 = z, s = fallback s-1), < 0 settled (-1 claimed,
+ * -2 dropped, -3 resolved by a re-check).  Each open request proposes to its
+ * current target (skipping full targets and targets that already hold x);
+ * every target accepts the proposal with the smallest pair index.
+ * d_best_scratch (node_count int32) must hold INT32_MAX and d_tgt_scratch
+ * (nreq int32) -1 on entry; both are restored.  *d_pending = open requests
+ * after the round, *d_dropped += requests that ran out of targets.  Only
+ * requests of nodes x < x_end take part (the reference visits x ascending),
+ * and per x only its lowest open pair index proposes (d_first_scratch:
+ * node_count int32 holding INT32_MAX, restored). */
+int ggnn_sym_claim_round(const int32_t *d_req, int64_t nreq, int32_t n_fallback, int32_t *d_adj,
+                         int32_t *d_sym_count, int32_t k, int32_t k_nn, int32_t *d_best_scratch, int32_t *d_stage,
+                         int32_t *d_tgt_scratch, int32_t *d_dropped, int32_t *d_pending, int32_t x_end,
+                         int32_t *d_first_scratch, void *stream);
+
+/* Re-check of open requests on the current graph (between claim rounds):
+ * for every r with d_stage[r] >= 0, re-runs the reachability search of
+ * sym_check_pair (_core.pyx:375-435) for (x, z, d_xz) of record r; settles it
+ * (d_stage[r] = -3) if the verdict is no longer 2, else refreshes its
+ * fallbacks in place.  Requests of nodes x >= x_end are skipped. */
+int ggnn_sym_recheck(const ggnn_vectors *X, const ggnn_layer *layer, int32_t *d_req, int64_t nreq, int32_t *d_stage,
+                     int32_t x_end, double tau, double d_nn1_max, int32_t budget, int32_t k_out, int32_t prioq_size,
+                     int32_t visited_size, int32_t n_fallback, void *stream);
 
 /* Replaces: compute_stats (build.py:275-280) / live_d_nn1_max
  * (graph.py:196-199): d_out[4] = {max of finite values (0 if none), sum of

@@ -84,18 +84,20 @@ class Workspace:
                                      device=dev)
         self.stats_out = t.empty((4,), dtype=t.float64, device=dev)
         self.best = t.full((n,), INT32_MAX, dtype=t.int32, device=dev)
+        self.first = t.full((n,), INT32_MAX, dtype=t.int32, device=dev)
         self.req_cap = 0
         self.req = self.stage = self.tgt = None
         self.req_count = t.zeros((1,), dtype=t.int32, device=dev)
         self.dropped = t.zeros((1,), dtype=t.int32, device=dev)
         self.reduced = t.zeros((1,), dtype=t.int32, device=dev)
+        self.pending = t.zeros((1,), dtype=t.int32, device=dev)
 
     def ensure_requests(self, cap: int, n_fallback: int):
         if cap > self.req_cap:
             t = N.torch()
             dev = N.device()
             self.req_cap = cap
-            self.req = t.empty((cap, 3 + n_fallback), dtype=t.int32, device=dev)
+            self.req = t.empty((cap, 5 + n_fallback), dtype=t.int32, device=dev)
             self.stage = t.empty((cap,), dtype=t.int32, device=dev)
             self.tgt = t.empty((cap,), dtype=t.int32, device=dev)
 

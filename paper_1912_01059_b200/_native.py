@@ -68,7 +68,8 @@ _SIGS = {
     "ggnn_merge_descent": [P, P, I32, I32, I32, P, I64, P, I32, I32, P, P, P, P, P],
     "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_sym_check_layer": [P, P, P, P, P, I32, F64, F64, I32, I32, I32, I32, I32, P, P, I64, P],
-    "ggnn_sym_claim": [P, P, I64, I32, P, P, I32, I32, P, P, P, P, P],
+    "ggnn_sym_claim_round": [P, I64, I32, P, P, I32, I32, P, P, P, P, P, I32, P, P],
+    "ggnn_sym_recheck": [P, P, P, I64, P, I32, F64, F64, I32, I32, I32, I32, I32, P],
     "ggnn_layer_stats": [P, I64, P, P, P],
     "ggnn_layer_stats_scratch_bytes": [],
 }

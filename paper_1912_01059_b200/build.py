@@ -27,8 +27,14 @@ SYM_CHECK_BUDGET = 16  # expansions allowed per reachability check (build.py:31)
 SYM_CHECK_PRIOQ = 64
 SYM_CHECK_VISITED = 128
 SYM_FALLBACK = 8
+# node windows per symmetrize pass: requests of x-window w are re-checked after the
+# claims of windows < w, approximating the reference's sequential x order
+SYM_WINDOWS = 16
 CONSENSUS_SAMPLE = 256
 CONSENSUS_K = 10
+
+# per-symmetrize-pass records when GGNN_TRACE is set (diagnostics)
+TRACE = [] if __import__("os").environ.get("GGNN_TRACE") else None
 
 
 def plan_geometry(n: int, s: int, g: int) -> tuple[int, int]:
@@ -210,8 +216,15 @@ def _merge_pass(h, j: int):
 
 
 def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
-    """symmetrize on the device: all reachability checks of the layer in one
-    launch, then the deterministic claim resolution.  Returns dropped links."""
+    """symmetrize on the device (build.py:200-266).
+
+    1. one launch checks every (x, z) pair of the layer on the current graph
+       and records the verdict-2 pairs as requests (pair-index priority);
+    2. claim rounds: every open request proposes to its current target and
+       each target accepts the lowest pair index; between rounds the open
+       requests are re-checked on the updated graph, so -- as in the
+       reference's sequential pass -- a link claimed earlier can make a later
+       request unnecessary.  Returns the number of dropped links."""
     G.ensure_device(h)
     layer = h.layers[j]
     dev = layer._dev
@@ -233,14 +246,33 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
         if cnt <= ws.req_cap:
             break
         ws.ensure_requests(2 * cnt, SYM_FALLBACK)  # checks do not mutate the layer: rerun
-    if cnt == 0:
-        return 0
-    ws.dropped.zero_()
-    N.call("ggnn_sym_claim", N.ptr(ws.req), N.ptr(ws.req_count), ws.req_cap, SYM_FALLBACK, N.ptr(dev["adj"]),
-           N.ptr(dev["symc"]), layer.k, layer.k_nn, N.ptr(ws.best), N.ptr(ws.stage), N.ptr(ws.tgt),
-           N.ptr(ws.dropped), N.stream_ptr())
-    layer._version += 1
-    return int(ws.dropped.item())
+    dropped = rounds = 0
+    if cnt:
+        ws.stage[:cnt].zero_()
+        ws.tgt[:cnt].fill_(-1)
+        ws.dropped.zero_()
+        nc = layer.node_count
+        windows = max(1, min(SYM_WINDOWS, cnt))
+        while True:
+            x_end = nc if rounds >= windows else (nc * (rounds + 1) + windows - 1) // windows
+            if rounds:
+                N.call("ggnn_sym_recheck", N.ctypes.byref(dv.struct), N.ctypes.byref(lstruct), N.ptr(ws.req), cnt,
+                       N.ptr(ws.stage), x_end, float(tau_build), d_max, SYM_CHECK_BUDGET, k_out, prioq,
+                       SYM_CHECK_VISITED, SYM_FALLBACK, N.stream_ptr())
+            N.call("ggnn_sym_claim_round", N.ptr(ws.req), cnt, SYM_FALLBACK, N.ptr(dev["adj"]), N.ptr(dev["symc"]),
+                   layer.k, layer.k_nn, N.ptr(ws.best), N.ptr(ws.stage), N.ptr(ws.tgt), N.ptr(ws.dropped),
+                   N.ptr(ws.pending), x_end, N.ptr(ws.first), N.stream_ptr())
+            rounds += 1
+            if x_end == nc and int(ws.pending.item()) == 0:
+                break
+        layer._version += 1
+        dropped = int(ws.dropped.item())
+    if TRACE is not None:
+        stage = ws.stage[:cnt].cpu().numpy() if cnt else np.zeros(0)
+        TRACE.append({"layer": j, "nodes": layer.node_count, "pairs": layer.node_count * per_node, "requests": cnt,
+                      "claimed": int((stage == -1).sum()), "resolved": int((stage == -3).sum()), "dropped": dropped,
+                      "rounds": rounds, "mean_sym": float(dev["symc"].double().mean().item())})
+    return dropped
 
 
 def _rescued_dict(resc) -> dict[int, list[tuple[int, float]]]:

@@ -288,6 +288,10 @@ __global__ void __launch_bounds__(256) descent_kernel(const __grid_constant__ Se
 }
 
 // ----------------------------------------------------------- sym_check_pair
+// Request records of a symmetrize pass (int32, stride REQ_HDR + n_fallback):
+//   {pair index p, x, z, d_xz low word, d_xz high word, fallback[n_fallback]}
+constexpr int REQ_HDR = 5;
+
 struct SymArgs {
   const void* X;
   int64_t d;
@@ -303,17 +307,23 @@ struct SymArgs {
   int n_fallback;
   int32_t* verdict;
   int32_t* fallback;
-  // layer-pairs mode (px == nullptr): pair p = x * per_node + t, t < k_nn is
-  // direct slot t of x (adj / nnd), t >= k_nn the (t - k_nn)-th rescued entry
+  // layer-pairs mode (px == nullptr, recheck == false): pair p = x * per_node + t,
+  // t < k_nn is direct slot t of x (adj / nnd), t >= k_nn the (t - k_nn)-th rescued entry
   const double* nnd;
   int k_nn;
   const int32_t* resc_id;
   const double* resc_d;
   int per_node;
-  // compact verdict-2 output: req[i] = {pair index, x, z, fb[n_fallback]}
+  // verdict-2 output (append) / recheck input
   int32_t* req;
   int32_t* req_count;
   int64_t req_cap;
+  // recheck mode: item i is request i; stage[i] < 0 means settled.  A request
+  // that is no longer verdict 2 on the current graph is settled as -3, else
+  // its fallbacks are refreshed from the new search.
+  bool recheck;
+  int32_t* stage;
+  int32_t x_end;  // recheck only requests of nodes x < x_end
 };
 
 template <typename TX>
@@ -324,9 +334,18 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
   const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (pi >= a.npairs) return;
   const int lane = lane_id();
+  const int rstride = REQ_HDR + a.n_fallback;
   int x, z;
   double dxz;
-  if (a.px) {
+  int32_t* rec = nullptr;
+  if (a.recheck) {
+    if (a.stage[pi] < 0) return;
+    rec = a.req + pi * rstride;
+    x = rec[1];
+    if (x >= a.x_end) return;
+    z = rec[2];
+    dxz = __hiloint2double(rec[4], rec[3]);
+  } else if (a.px) {
     x = __ldg(a.px + pi);
     z = __ldg(a.pz + pi);
     dxz = a.pd[pi];
@@ -350,41 +369,33 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
   // verdict 0: x already sits in one of z's slots (_core.pyx:405-408)
   int slot = lane < a.layer.k ? __ldg(a.layer.adj + (int64_t)z * a.layer.k + lane) : -1;
   const bool present = __any_sync(FULL, slot == x);
-  if (present) {
-    if (lane == 0 && a.verdict) a.verdict[pi] = 0;
-    if (fb)
-      for (int j = lane; j < a.n_fallback; j += 32) fb[j] = -1;
-    return;
-  }
-  WarpSearch<TX, TX> s;
-  s.X = reinterpret_cast<const TX*>(a.X);
-  s.d = a.d;
-  s.lpr = a.lpr;
-  s.c = a.c;
-  s.target = x;
-  s.carve(smem + (size_t)wib * a.region);
-  s.ever = nullptr;
-  s.ever_mask = 0;
-  set_layer(s, a.layer);
-  s.dmax = a.dmax;
-  const int xrow = a.layer.to_row ? __ldg(a.layer.to_row + x) : x;
-  const TX* src = s.X + (int64_t)xrow * a.d;
-  for (int64_t e = lane; e < a.d; e += 32) s.qs[e] = src[e];
-  __syncwarp();
-  s.reset();
-  s.seed(KeyOps<Key>::from_d(dxz), lane == 0 ? z : -1, 1);
-  s.run();
-  const int v = s.term ? 1 : 2;
-  if (lane == 0 && a.verdict) a.verdict[pi] = v;
-  if (v != 2) {
-    if (fb)
-      for (int j = lane; j < a.n_fallback; j += 32) fb[j] = -1;
-    return;
-  }
-  // fallbacks: closest explored ids excluding x and z (_core.pyx:420-426)
+  int v = 0;
   int cand = -1;
-  const int nh = min(s.L, a.c.k_out);
-  if (lane < nh) cand = s.rid[lane];
+  WarpSearch<TX, TX> s;
+  if (!present) {
+    s.X = reinterpret_cast<const TX*>(a.X);
+    s.d = a.d;
+    s.lpr = a.lpr;
+    s.c = a.c;
+    s.target = x;
+    s.carve(smem + (size_t)wib * a.region);
+    s.ever = nullptr;
+    s.ever_mask = 0;
+    set_layer(s, a.layer);
+    s.dmax = a.dmax;
+    const int xrow = a.layer.to_row ? __ldg(a.layer.to_row + x) : x;
+    const TX* src = s.X + (int64_t)xrow * a.d;
+    for (int64_t e = lane; e < a.d; e += 32) s.qs[e] = src[e];
+    __syncwarp();
+    s.reset();
+    s.seed(KeyOps<Key>::from_d(dxz), lane == 0 ? z : -1, 1);
+    s.run();
+    v = s.term ? 1 : 2;
+    // fallbacks: closest explored ids excluding x and z (_core.pyx:420-426)
+    const int nh = min(s.L, a.c.k_out);
+    if (v == 2 && lane < nh) cand = s.rid[lane];
+  }
+  if (lane == 0 && a.verdict) a.verdict[pi] = v;
   const bool keep = cand >= 0 && cand != x && cand != z;
   const unsigned km = __ballot_sync(FULL, keep);
   const int rank = __popc(km & lanemask_lt());
@@ -393,21 +404,29 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
     if (keep && rank < a.n_fallback) fb[rank] = cand;
     for (int j = w + lane; j < a.n_fallback; j += 32) fb[j] = -1;
   }
-  if (a.req) {
+  if (a.recheck) {
+    if (v != 2) {
+      if (lane == 0) a.stage[pi] = -3;
+      return;
+    }
+  } else if (v == 2 && a.req) {
     int slot_i = 0;
     if (lane == 0) slot_i = atomicAdd(a.req_count, 1);
     slot_i = __shfl_sync(FULL, slot_i, 0);
-    if (slot_i < a.req_cap) {
-      int32_t* r = a.req + (int64_t)slot_i * (3 + a.n_fallback);
-      if (lane == 0) {
-        r[0] = (int32_t)pi;
-        r[1] = x;
-        r[2] = z;
-      }
-      if (keep && rank < a.n_fallback) r[3 + rank] = cand;
-      for (int j = w + lane; j < a.n_fallback; j += 32) r[3 + j] = -1;
+    if (slot_i >= a.req_cap) return;
+    rec = a.req + (int64_t)slot_i * rstride;
+    if (lane == 0) {
+      rec[0] = (int32_t)pi;
+      rec[1] = x;
+      rec[2] = z;
+      rec[3] = __double2loint(dxz);
+      rec[4] = __double2hiint(dxz);
     }
+  } else {
+    return;
   }
+  if (keep && rank < a.n_fallback) rec[REQ_HDR + rank] = cand;
+  for (int j = w + lane; j < a.n_fallback; j += 32) rec[REQ_HDR + j] = -1;
 }
 
 // ----------------------------------------------------------- exhaustive_topk
@@ -767,6 +786,46 @@ int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const d
   size_t smem = (size_t)W * a.region;
   cudaStream_t st = as_stream(stream);
   int64_t grid = (npairs + W - 1) / W;
+  if (X->dtype == GGNN_U8) {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);
+  } else {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    symcheck_kernel<float><<<(unsigned)grid, W * 32, smem, st>>>(a);
+  }
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_req, int64_t nreq,
+                      int32_t* d_stage, int32_t x_end, double tau, double d_nn1_max, int32_t budget, int32_t k_out,
+                      int32_t prioq_size, int32_t visited_size, int32_t n_fallback, void* stream) {
+  GGNN_CHECK_ARG(X && X->d_data && layer && layer->d_adj && d_req && d_stage, "invalid arguments");
+  GGNN_CHECK_ARG(layer->k >= 1 && layer->k <= MAX_K, "invalid layer geometry");
+  GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32 && n_fallback >= 0 && n_fallback <= 32, "k_out / n_fallback in [1, 32]");
+  if (nreq <= 0) return GGNN_OK;
+  SymArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = X->d_data;
+  a.d = X->d;
+  a.lpr = choose_lpr(X->d, X->dtype, X->dtype, reinterpret_cast<uintptr_t>(X->d_data));
+  a.layer = to_dev(*layer);
+  a.npairs = nreq;
+  ggnn_search_params p{k_out, prioq_size, visited_size, 0, tau, budget};
+  a.c = make_cfg(&p);
+  a.dmax = d_nn1_max;
+  a.n_fallback = n_fallback;
+  a.req = d_req;
+  a.recheck = true;
+  a.stage = d_stage;
+  a.x_end = x_end;
+  int keysize = X->dtype == GGNN_U8 ? 4 : 8;
+  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
+  int W = pick_warps(a.region, 8);
+  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
+  size_t smem = (size_t)W * a.region;
+  cudaStream_t st = as_stream(stream);
+  int64_t grid = (nreq + W - 1) / W;
   if (X->dtype == GGNN_U8) {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);

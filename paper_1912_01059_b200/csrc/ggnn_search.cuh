@@ -93,6 +93,7 @@ struct WarpSearch {
   // warp-uniform state
   int L, vlen, vpos, used;
   int visited, steps, distinct, forgotten, term;
+  bool found_target;
 
   __device__ void carve(uint8_t* base) {
     uint8_t* p = base;
@@ -122,6 +123,7 @@ struct WarpSearch {
     L = vlen = vpos = used = 0;
     visited = steps = distinct = forgotten = 0;
     term = TERM_EMPTY;
+    found_target = false;
   }
 
   __device__ __forceinline__ int ever_insert(int id) {
@@ -344,6 +346,7 @@ struct WarpSearch {
     }
     steps++;
     if (found) {
+      found_target = true;  // _core.pyx:309-311 returns here with term = 1
       term = 1;
       return false;
     }
@@ -353,7 +356,7 @@ struct WarpSearch {
   __device__ void run() {
     while (step()) {
     }
-    if (target >= 0 && term != 1) term = 0;
+    if (target >= 0) term = found_target ? 1 : 0;  // _core.pyx:311-312
   }
 
   // first min(L, k_out) ring entries -> ids / keys in lanes (k_out <= 32)

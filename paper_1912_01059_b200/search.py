@@ -239,3 +239,17 @@ def exact_knn_rows(dataset, rows: np.ndarray, k: int):
     N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), N.ptr(ids),
            N.ptr(dists), N.stream_ptr())
     return ids.cpu().numpy(), dists.cpu().numpy()
+
+
+def exact_knn(dataset, queries: np.ndarray, k: int):
+    """Exact top-k (k <= 32) of external queries against the whole dataset,
+    ties by ascending id (ground truth for recall), one launch."""
+    dv = DeviceVectors.of(dataset)
+    dq, qs = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
+    t = N.torch()
+    m = qs.m
+    ids = N.empty((m, k), t.int32)
+    dists = N.empty((m, k), t.float64)
+    N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), N.ptr(ids),
+           N.ptr(dists), N.stream_ptr())
+    return ids.cpu().numpy(), dists.cpu().numpy()
