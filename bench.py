@@ -97,6 +97,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.rows = []
         self.proc = None
+        self.first = threading.Event()
 
     def __enter__(self):
         try:
@@ -112,6 +113,13 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
+            self.first.set()
+
+    def wait_first(self, timeout: float = 5.0):
+        """Block until nvidia-smi has produced its first sample (it takes a
+        few hundred ms to start), so the samples cover the timed region."""
+        if self.proc is not None:
+            self.first.wait(timeout)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -296,14 +304,22 @@ def main():
                N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, N.ptr(ids),
                N.ptr(dists), N.ptr(cnt), None, 0, N.stream_ptr())
 
-    for _ in range(args.warmup):
-        step()
     stream = torch.cuda.current_stream()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clocks:
+        clocks.wait_first()
+        # warm-up: at least W steps, and at least 0.5 s of load so the clock
+        # samples see the GPU busy before the timed region starts
+        t_w = time.perf_counter()
+        done = 0
+        while done < args.warmup or time.perf_counter() - t_w < 0.5:
+            step()
+            done += 1
+            if done % 8 == 0:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
         evs[0].record(stream)
         for i in range(args.steps):
             step()

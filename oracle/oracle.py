@@ -163,3 +163,22 @@ def query(layers, to_bottom, X, q, k_out, tau, d_nn1_max, max_iterations=1000, p
         X, np.arange(X.shape[0], dtype=np.int32), adj, k_nn, symc, q, seeds, sd, k_out, tau, d_nn1_max,
         max_iterations, prioq_size, visited_size)
     return ids, dists, v + len(top_rows), t, term, distinct + len(top_rows) - len(seeds), forgotten
+
+
+def merge_shard_results(parts, permutation, k_out):
+    """_merge_shard_results (shard.py:91-110): `parts` is a list of
+    (offset, ids, dists, visited, steps, term_code) per shard with shard-local
+    ids; returns (global ids, dists, visited sum, steps sum, term of the best
+    hit's shard or 1 (queue-empty) when nothing was found)."""
+    pairs = []
+    visited = steps = 0
+    for offset, ids, dists, v, t, term in parts:
+        for local, dist in zip(ids, dists):
+            pairs.append((float(dist), int(permutation[offset + int(local)]), int(term)))
+        visited += int(v)
+        steps += int(t)
+    pairs.sort(key=lambda p: (p[0], p[1]))
+    top = pairs[:k_out]
+    term = top[0][2] if top else TERM_QUEUE_EMPTY
+    return (np.array([p[1] for p in top], dtype=np.int32), np.array([p[0] for p in top], dtype=np.float64),
+            visited, steps, term)

@@ -35,4 +35,17 @@ from .build import (
     symmetrize,
 )
 
+from .evaluate import GroundTruth, brute_force_oracle, consensus_at_k, k_recall_at, oracle_knn_graph, recall_at
+from .index_file import IndexFormatError, load_index, save_index
+from .shard import (
+    ShardedIndex,
+    batch_query_sharded,
+    build_sharded,
+    load_sharded,
+    query_sharded,
+    query_sharded_arrays,
+    query_sharded_sequential,
+    save_sharded,
+)
+
 __version__ = "0.1.0"

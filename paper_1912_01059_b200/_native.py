@@ -72,9 +72,15 @@ _SIGS = {
     "ggnn_sym_recheck": [P, P, P, I64, P, I32, F64, F64, I32, I32, I32, I32, I32, P],
     "ggnn_layer_stats": [P, I64, P, P, P],
     "ggnn_layer_stats_scratch_bytes": [],
+    "ggnn_shard_block_bytes": [I64, I32],
+    "ggnn_shard_block_dists_offset": [I64, I32],
+    "ggnn_shard_block_counters_offset": [I64, I32],
+    "ggnn_shard_globalize": [P, I64, P, I64, P],
+    "ggnn_shard_merge": [P, I32, I64, I32, I32, P, P, P, P],
 }
 _RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t,
-             "ggnn_layer_stats_scratch_bytes": ctypes.c_size_t}
+             "ggnn_layer_stats_scratch_bytes": ctypes.c_size_t, "ggnn_shard_block_bytes": ctypes.c_size_t,
+             "ggnn_shard_block_dists_offset": ctypes.c_size_t, "ggnn_shard_block_counters_offset": ctypes.c_size_t}
 # entry points added by later translation units register themselves here
 EXTRA_SIGS: dict = {}
 

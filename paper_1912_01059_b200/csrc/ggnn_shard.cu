@@ -1,0 +1,161 @@
+// ggnn_shard.cu -- id globalization and the exact G-way merge of per-shard
+// top-k lists (the reference's _merge_shard_results, shard.py:91-110).
+//
+// One warp per query: the G * k_in candidates of the query are streamed
+// through the warp 32 at a time and folded into a running ascending top-32
+// by the bitonic merge of search.cuh (topk_merge_chunk), keyed by
+// (distance f64, dataset id) -- the reference's sort key (shard.py:106).
+// The per-shard lists are already ascending, so the first entry of the list
+// that supplies the overall best hit identifies its shard (ids of different
+// shards are disjoint), which gives terminated_by (shard.py:108).
+#include <climits>
+#include "ggnn_capi_util.cuh"
+#include "ggnn_search.cuh"
+#include "ggnn_shard.h"
+
+namespace ggnn {
+namespace {
+
+__host__ __device__ inline size_t block_dists_off(int64_t m, int k_in) {
+  return (((size_t)m * k_in * 4) + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t block_cnt_off(int64_t m, int k_in) {
+  return block_dists_off(m, k_in) + (size_t)m * k_in * 8;
+}
+__host__ __device__ inline size_t block_bytes(int64_t m, int k_in) {
+  return (block_cnt_off(m, k_in) + (size_t)m * 5 * 4 + 255) & ~size_t(255);
+}
+
+__global__ void globalize_kernel(int32_t* ids, int64_t count, const int32_t* gid, int64_t size) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = ids[i];
+    if (v >= 0 && v < size) ids[i] = __ldg(gid + v);
+  }
+}
+
+struct MergeShardArgs {
+  const uint8_t* blocks;
+  size_t block_bytes, dists_off, cnt_off;
+  int G;
+  int64_t m;
+  int k_in, k_out;
+  int32_t* out_ids;
+  double* out_dists;
+  int32_t* out_cnt;
+};
+
+__global__ void __launch_bounds__(256) shard_merge_kernel(const __grid_constant__ MergeShardArgs a) {
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= a.m) return;
+  const int lane = lane_id();
+  using KO = KeyOps<double>;
+  double bk = KO::max_key();
+  int bi = INT_MAX;
+  const int total = a.G * a.k_in;
+  long long vsum = 0, tsum = 0;
+  for (int base = 0; base < total; base += 32) {
+    const int e = base + lane;
+    double ck = KO::max_key();
+    int cx = INT_MAX;
+    if (e < total) {
+      const int g = e / a.k_in, j = e - g * a.k_in;
+      const uint8_t* blk = a.blocks + (size_t)g * a.block_bytes;
+      const int32_t id = reinterpret_cast<const int32_t*>(blk)[q * a.k_in + j];
+      if (id >= 0) {
+        ck = reinterpret_cast<const double*>(blk + a.dists_off)[q * a.k_in + j];
+        cx = id;
+      }
+    }
+    topk_merge_chunk(bk, bi, ck, cx, a.k_out);
+  }
+  if (a.out_cnt) {
+    for (int g = lane; g < a.G; g += 32) {
+      const int32_t* c = reinterpret_cast<const int32_t*>(a.blocks + (size_t)g * a.block_bytes + a.cnt_off) + q * 5;
+      vsum += c[0];
+      tsum += c[1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      vsum += __shfl_xor_sync(FULL, vsum, o);
+      tsum += __shfl_xor_sync(FULL, tsum, o);
+    }
+  }
+  const int best = __shfl_sync(FULL, bi, 0);
+  if (lane < a.k_out) {
+    const bool ok = bi != INT_MAX;
+    a.out_ids[q * a.k_out + lane] = ok ? bi : -1;
+    a.out_dists[q * a.k_out + lane] = ok ? bk : KO::max_key();
+  }
+  if (a.out_cnt) {
+    int term = TERM_EMPTY;  // shard.py:108 "queue-empty" when nothing was found
+    if (best != INT_MAX) {
+      // exactly one shard list starts with `best` (shard ids are disjoint)
+      int src = -1;
+      for (int g0 = 0; g0 < a.G && src < 0; g0 += 32) {
+        const int g = g0 + lane;
+        bool hit = false;
+        if (g < a.G) hit = reinterpret_cast<const int32_t*>(a.blocks + (size_t)g * a.block_bytes)[q * a.k_in] == best;
+        const unsigned bal = __ballot_sync(FULL, hit);
+        if (bal) src = g0 + __ffs(bal) - 1;
+      }
+      if (src >= 0)
+        term = reinterpret_cast<const int32_t*>(a.blocks + (size_t)src * a.block_bytes + a.cnt_off)[q * 5 + 2];
+    }
+    if (lane == 0) {
+      int32_t* c = a.out_cnt + q * 5;
+      c[0] = (int32_t)vsum;
+      c[1] = (int32_t)tsum;
+      c[2] = term;
+      c[3] = 0;
+      c[4] = 0;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace ggnn
+
+using namespace ggnn;
+
+extern "C" size_t ggnn_shard_block_bytes(int64_t m, int32_t k_in) { return block_bytes(m, k_in); }
+extern "C" size_t ggnn_shard_block_dists_offset(int64_t m, int32_t k_in) { return block_dists_off(m, k_in); }
+extern "C" size_t ggnn_shard_block_counters_offset(int64_t m, int32_t k_in) { return block_cnt_off(m, k_in); }
+
+extern "C" int ggnn_shard_globalize(int32_t* d_ids, int64_t count, const int32_t* d_gid_of_local, int64_t size,
+                                    void* stream) {
+  GGNN_CHECK_ARG(count >= 0 && size >= 0, "ggnn_shard_globalize: negative size");
+  if (count == 0) return GGNN_OK;
+  GGNN_CHECK_ARG(d_ids && d_gid_of_local, "ggnn_shard_globalize: null pointer");
+  const int threads = 256;
+  const int64_t want = (count + threads - 1) / threads;
+  const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
+  globalize_kernel<<<blocks, threads, 0, as_stream(stream)>>>(d_ids, count, d_gid_of_local, size);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+extern "C" int ggnn_shard_merge(const void* d_blocks, int32_t G, int64_t m, int32_t k_in, int32_t k_out,
+                                int32_t* d_out_ids, double* d_out_dists, int32_t* d_out_counters, void* stream) {
+  GGNN_CHECK_ARG(G >= 1 && m >= 0 && k_in >= 1, "ggnn_shard_merge: bad shape G=%d m=%lld k_in=%d", G, (long long)m,
+                 k_in);
+  GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32, "ggnn_shard_merge: k_out must be in [1, 32], got %d", k_out);
+  if (m == 0) return GGNN_OK;
+  GGNN_CHECK_ARG(d_blocks && d_out_ids && d_out_dists, "ggnn_shard_merge: null pointer");
+  MergeShardArgs a;
+  a.blocks = static_cast<const uint8_t*>(d_blocks);
+  a.block_bytes = block_bytes(m, k_in);
+  a.dists_off = block_dists_off(m, k_in);
+  a.cnt_off = block_cnt_off(m, k_in);
+  a.G = G;
+  a.m = m;
+  a.k_in = k_in;
+  a.k_out = k_out;
+  a.out_ids = d_out_ids;
+  a.out_dists = d_out_dists;
+  a.out_cnt = d_out_counters;
+  const int wpb = 8;
+  const int64_t blocks = (m + wpb - 1) / wpb;
+  shard_merge_kernel<<<(unsigned)blocks, wpb * 32, 0, as_stream(stream)>>>(a);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}

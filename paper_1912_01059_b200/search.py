@@ -125,6 +125,20 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
     return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())
 
 
+def launch_query(h, queries: np.ndarray, cfg: QueryConfig, ids_p, dists_p, cnt_p) -> None:
+    """One ggnn_query_batch launch of every row of `queries` on hierarchy h,
+    writing into caller-owned device memory (ids int32 / dists f64 (m, k_out),
+    counters int32 (m, 5)); distinct_touched is not computed."""
+    dh = device_hierarchy(h)
+    dv = dh.vectors
+    dq, qs = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
+    params = _params(cfg, _flags(dv, False))
+    N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct), N.ptr(dh.top_rows),
+           dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, ids_p, dists_p, cnt_p, None, 0,
+           N.stream_ptr())
+    del dq
+
+
 def query(h, q: np.ndarray, cfg: QueryConfig | None = None) -> QueryResult:
     """Top-to-bottom jump: brute-force the top layer, then search the bottom
     (search.py:115-137)."""

@@ -20,6 +20,12 @@ Fixtures:
   sift10k.npz       make_sift_shaped 10k x 128 built with BuildConfig(seed=7)
                     (tests/conftest.py:125-129); layers, stats, and query()
                     results for 100 queries at tau 0.3/0.6/0.8, k_out=10.
+  ref_int.idx       the kernels_int.npz hierarchy written by the reference's
+                    save_index (GGNN v1 bytes, index_file.py:55-91).
+  sharded_int.npz   reference build_sharded of the kernels_int data
+                    (shard_size 250 -> 3 shards), every shard's graph, the
+                    permutation, and query_sharded results (ids, dists,
+                    visited, steps, term) for the kernels_int queries.
 """
 
 from __future__ import annotations
@@ -160,18 +166,46 @@ def make_sift10k(R):
     print("sift10k.npz build", stats.build_seconds, "s")
 
 
+def make_index_and_sharded(R):
+    g = np.load(OUT / "kernels_int.npz")
+    X, Q = g["X"], g["Q"]
+    cfg = R.BuildConfig(k=8, k_nn=4, k_sym=4, s=16, g=2, refinements=1, seed=13)
+    h, _ = R.build(R.Dataset(X.copy()), cfg)
+    assert np.array_equal(h.layers[0].adjacency, g["adj0"]), "reference build is not reproducible"
+    R.save_index(h, OUT / "ref_int.idx")
+    si, _ = R.build_sharded(R.Dataset(X.copy()), 250, cfg)
+    out = {"perm": si.permutation, "offsets": np.array([o for o, _ in si.shards], dtype=np.int64),
+           "shard_size": np.int64(si.shard_size)}
+    for i, (_, hs) in enumerate(si.shards):
+        out.update(graph_arrays(hs, prefix=f"s{i}_"))
+    qc = R.QueryConfig(k_out=6, tau=0.6)
+    term_code = {"stopping-rule": 0, "queue-empty": 1, "iteration-cap": 2}
+    ids = np.full((len(Q), 6), -1, dtype=np.int32)
+    dists = np.full((len(Q), 6), np.inf)
+    cnt = np.zeros((len(Q), 3), dtype=np.int64)
+    for i, q in enumerate(Q):
+        r = R.query_sharded(si, q, qc)
+        ids[i, : len(r.ids)], dists[i, : len(r.dists)] = r.ids, r.dists
+        cnt[i] = [r.visited_count, r.steps, term_code[r.terminated_by]]
+    out["q_ids"], out["q_dists"], out["q_cnt"] = ids, dists, cnt
+    np.savez_compressed(OUT / "sharded_int.npz", **out)
+    print("ref_int.idx", (OUT / "ref_int.idx").stat().st_size, "bytes; sharded_int.npz", len(si.shards), "shards")
+
+
 def main():
     R = O.reference_module()
     if R is None:
         raise SystemExit("run oracle/build_ref.sh first (needs /root/reference)")
     assert R.backend.BACKEND == "compiled"
-    which = sys.argv[1:] or ["int", "float", "sift"]
+    which = sys.argv[1:] or ["int", "float", "sift", "index"]
     if "int" in which:
         make_kernels_int(R)
     if "float" in which:
         make_float_small(R)
     if "sift" in which:
         make_sift10k(R)
+    if "index" in which:
+        make_index_and_sharded(R)
 
 
 if __name__ == "__main__":

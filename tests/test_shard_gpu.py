@@ -1,0 +1,142 @@
+"""Sharded search on the GPU vs the reference (same graphs) and vs the CPU
+checker (merge kernel), plus index persistence round trips of GPU graphs."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1912_01059_b200 as ga
+from paper_1912_01059_b200 import _native as N
+from paper_1912_01059_b200.shard import block_layout, merge_blocks
+from test_persist import _golden_shards
+
+pytestmark = pytest.mark.gpu
+
+
+def test_same_graph_sharded_query_bitwise():
+    """Reference-built shards queried on the GPU: ids, dists, visited, steps
+    and terminated_by equal the reference's query_sharded (shard.py:113-128)."""
+    g, X, si = _golden_shards()
+    from conftest import load_golden
+
+    Q = load_golden("kernels_int.npz")["Q"]
+    res = ga.query_sharded_arrays(si, Q, ga.QueryConfig(k_out=6, tau=0.6))
+    np.testing.assert_array_equal(res.ids, g["q_ids"])
+    np.testing.assert_array_equal(res.dists, g["q_dists"])
+    np.testing.assert_array_equal(res.counters[:, :3], g["q_cnt"])
+    one = ga.query_sharded(si, Q[3], ga.QueryConfig(k_out=6, tau=0.6))
+    np.testing.assert_array_equal(one.ids, g["q_ids"][3][g["q_ids"][3] >= 0])
+
+
+@pytest.mark.parametrize("G,k_in,k_out", [(1, 10, 10), (3, 6, 6), (8, 10, 10), (5, 24, 24), (9, 12, 7), (40, 4, 32)])
+def test_merge_kernel_vs_oracle(G, k_in, k_out):
+    rng = np.random.default_rng(G * 100 + k_in)
+    m = 257
+    bb, doff, coff = block_layout(m, k_in)
+    raw = np.zeros(G * bb, dtype=np.uint8)
+    n_total = G * 1000
+    ident = np.arange(n_total, dtype=np.int32)
+    gids = rng.permutation(n_total).astype(np.int32).reshape(G, 1000)
+    parts_all = [[] for _ in range(m)]
+    for gi in range(G):
+        blk = raw[gi * bb:(gi + 1) * bb]
+        ids = blk[: m * k_in * 4].view(np.int32).reshape(m, k_in)
+        ds = blk[doff: doff + m * k_in * 8].view(np.float64).reshape(m, k_in)
+        cnt = blk[coff: coff + m * 20].view(np.int32).reshape(m, 5)
+        for i in range(m):
+            nh = int(rng.integers(0, k_in + 1)) if i % 7 == 0 else k_in
+            d = np.sort(rng.integers(0, 40, size=nh).astype(np.float64))  # heavy cross-shard ties
+            sel = rng.choice(1000, size=nh, replace=False)
+            idl = gids[gi, sel]
+            order = np.lexsort((idl, d))
+            ids[i] = -1
+            ds[i] = np.inf
+            ids[i, :nh] = idl[order]
+            ds[i, :nh] = d[order]
+            cnt[i] = [int(rng.integers(0, 999)), int(rng.integers(0, 99)), int(rng.integers(0, 3)), 5, 5]
+            parts_all[i].append((0, ids[i, :nh].copy(), ds[i, :nh].copy(), cnt[i, 0], cnt[i, 1], cnt[i, 2]))
+    buf = N.to_dev(raw)
+    ids, dists, cnt = merge_blocks(buf, G, m, k_in, k_out)
+    ids, dists, cnt = ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy()
+    for i in range(m):
+        gi_, gd, v, t, term = O.merge_shard_results(parts_all[i], ident, k_out)
+        nh = len(gi_)
+        np.testing.assert_array_equal(ids[i, :nh], gi_)
+        np.testing.assert_array_equal(dists[i, :nh], gd)
+        assert (ids[i, nh:] == -1).all() and np.isinf(dists[i, nh:]).all()
+        assert tuple(cnt[i]) == (v, t, term, 0, 0)
+
+
+def test_gpu_built_shards_merge_exact_and_persist(tmp_path):
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, Q = make_latent16(n=3000, d=32, m=200, seed=3)
+    ds = ga.Dataset(base)
+    cfg = ga.BuildConfig(seed=7)
+    si, stats = ga.build_sharded(ds, 1100, cfg)
+    assert [o for o, _ in si.shards] == [0, 1100, 2200] and len(stats) == 3
+    qc = ga.QueryConfig(k_out=10, tau=0.6)
+    res = ga.query_sharded_arrays(si, Q, qc)
+    # oracle-substituted merge of the per-shard GPU answers (test_shard.py:78-97)
+    per = [ga.query_arrays(h, Q, qc) for _, h in si.shards]
+    for i in range(len(Q)):
+        parts = []
+        for (off, h), r in zip(si.shards, per):
+            keep = r.ids[i] >= 0
+            parts.append((off, r.ids[i][keep], r.dists[i][keep], r.counters[i, 0], r.counters[i, 1],
+                          r.counters[i, 2]))
+        gi, gd, v, t, term = O.merge_shard_results(parts, si.permutation, 10)
+        np.testing.assert_array_equal(res.ids[i, :len(gi)], gi)
+        np.testing.assert_array_equal(res.dists[i, :len(gd)], gd)
+        assert tuple(res.counters[i, :3]) == (v, t, term)
+    gt = ga.brute_force_oracle(ds, Q, 10)
+    assert ga.recall_at(res.ids, gt.ids[:, 0], 10) >= 0.95
+    # persistence: the sequential (one shard resident at a time) path answers identically
+    ga.save_sharded(si, tmp_path / "sh")
+    seq = ga.shard.query_sharded_sequential_arrays(tmp_path / "sh", ds, Q, qc)
+    np.testing.assert_array_equal(seq.ids, res.ids)
+    np.testing.assert_array_equal(seq.dists, res.dists)
+    back = ga.load_sharded(tmp_path / "sh", ds)
+    np.testing.assert_array_equal(ga.query_sharded_arrays(back, Q, qc).ids, res.ids)
+
+
+def test_gpu_built_index_save_load_query(tmp_path):
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, Q = make_latent16(n=2500, d=64, m=100, seed=9)
+    ds = ga.Dataset(base)
+    h, _ = ga.build(ds, ga.BuildConfig(seed=7))
+    qc = ga.QueryConfig(k_out=10, tau=0.5)
+    a = ga.query_arrays(h, Q, qc)
+    ga.save_index(h, tmp_path / "g.idx")
+    h2 = ga.load_index(tmp_path / "g.idx").attach(ds)
+    b = ga.query_arrays(h2, Q, qc)
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dists, b.dists)
+    np.testing.assert_array_equal(a.counters, b.counters)
+    # and the CPU checker, querying the loaded file's graph, agrees bit for bit
+    layers = [(L.adjacency, L.k_nn, L.sym_count) for L in h2.layers]
+    for i in range(0, 100, 7):
+        ids, dd, v, t, term, _, _ = O.query(layers, h2.to_bottom, base, Q[i], 10, 0.5, h2.stats.d_nn1_max)
+        np.testing.assert_array_equal(a.ids[i, :len(ids)], ids)
+        assert (a.counters[i, 0], a.counters[i, 1], a.counters[i, 2]) == (v, t, term)
+
+
+def test_brute_force_oracle_and_knn_graph():
+    rng = np.random.default_rng(1)
+    X = rng.integers(0, 8, size=(700, 6)).astype(np.float32)
+    ds = ga.Dataset(X)
+    Q = rng.integers(0, 8, size=(50, 6)).astype(np.float32)
+    gt = ga.brute_force_oracle(ds, Q, 7)
+    for i in range(50):
+        ids, d = O.exhaustive_topk(X, Q[i], 7)
+        np.testing.assert_array_equal(gt.ids[i], ids)
+        np.testing.assert_array_equal(gt.dists[i], d)
+    with pytest.raises(ValueError):
+        ga.brute_force_oracle(ds, Q, 10_000)
+    kg = ga.oracle_knn_graph(ds, 3)
+    for i in range(0, 700, 37):
+        ids, _ = O.exhaustive_topk(X, X[i], 4)
+        np.testing.assert_array_equal(kg[i], [v for v in ids if v != i][:3])
