@@ -42,15 +42,19 @@ def up_to_date() -> bool:
     return LIB.exists() and stamp.exists() and stamp.read_text().strip() == _digest()
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    if not force and up_to_date():
+def build(verbose: bool = False, force: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Build the library (in-tree by default).  `out` + `defines` produce an
+    alternative build (e.g. -DGGNN_U8_UNR=4) for A/B runs via GGNN_LIB."""
+    lib = Path(out) if out is not None else LIB
+    if out is None and not defines and not force and up_to_date():
         return LIB
-    OBJ.mkdir(parents=True, exist_ok=True)
+    obj_dir = OBJ if out is None else OBJ / Path(out).stem
+    obj_dir.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
 
     def compile_one(src: Path) -> Path:
-        obj = OBJ / (src.stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -62,14 +66,15 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
         objs = list(pool.map(compile_one, srcs))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    LIB.with_suffix(".so.stamp").write_text(_digest())
-    return LIB
+    os.replace(tmp, lib)
+    if out is None and not defines:
+        LIB.with_suffix(".so.stamp").write_text(_digest())
+    return lib
 
 
 if __name__ == "__main__":

@@ -13,7 +13,8 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libggnn_b200.so"
+# GGNN_LIB overrides the library path (A/B experiments with alternative builds)
+LIB_PATH = Path(__import__("os").environ.get("GGNN_LIB", PKG / "libggnn_b200.so"))
 
 GGNN_F32 = 0
 GGNN_U8 = 1

@@ -243,6 +243,29 @@ __device__ __forceinline__ void warp_dists(const TX* X, int64_t d, const TQ* qs,
   dists_scalar<TX, TQ>(X, d, qs, rows, cnt, kout);
 }
 
+// Compile-time lanes-per-row dispatch: LP > 0 selects one vectorised variant
+// (so a kernel instantiated for LP carries only that variant's registers),
+// LP == 0 keeps the runtime switch above.  LP must equal choose_lpr(...) of
+// the launch; mixed u8-data / float-query searches always use LP == 0.
+#ifndef GGNN_U8_UNR
+#define GGNN_U8_UNR 4  // rows per lane group in flight for 128-byte uint8 rows (8 spills at 80 regs)
+#endif
+template <typename TX, typename TQ, int LP>
+__device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
+                                             typename VecTraits<TX, TQ>::Key* kout, int lpr) {
+  if constexpr (LP == 8 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
+    dists_u8_vec<8, GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
+  } else if constexpr (LP == 32 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
+    dists_u8_vec<32, 4>(X, d, qs, rows, cnt, kout);
+  } else if constexpr (LP == 8 && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {
+    dists_f32_vec<8, 4>(X, d, qs, rows, cnt, kout);
+  } else if constexpr (LP == 32 && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {
+    dists_f32_vec<32, 4>(X, d, qs, rows, cnt, kout);
+  } else {
+    warp_dists<TX, TQ>(X, d, qs, rows, cnt, kout, lpr);
+  }
+}
+
 // Lanes-per-row code for the vectorised paths (0 = scalar fallback).
 inline int choose_lpr(int64_t d, int dtype_x, int dtype_q, uintptr_t base) {
   int chunk = 0;

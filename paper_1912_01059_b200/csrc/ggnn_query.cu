@@ -39,6 +39,14 @@ DevInfo dev_info() {
 }
 
 constexpr int MAX_LAYERS = 24;
+// Search CTAs: up to 4 warps (one search each); 6 resident CTAs per SM caps
+// registers at 80 per thread, so 24 searches share an SM (shared memory
+// allows about as many for the default 266-entry ring + 512-entry visited
+// ring + 1024-slot table).  Sym-check CTAs run 8 warps of small searches.
+constexpr int SEARCH_THREADS = 128;
+constexpr int SEARCH_MIN_BLOCKS = 6;
+constexpr int SYM_THREADS = 256;
+constexpr int SYM_MIN_BLOCKS = 3;
 
 struct LayerDev {
   const int32_t* adj;
@@ -98,8 +106,8 @@ __device__ __forceinline__ void load_query(TQ* qs, const SearchArgs& a, int64_t 
   __syncwarp();
 }
 
-template <typename TX, typename TQ>
-__device__ __forceinline__ void init_search(WarpSearch<TX, TQ>& s, const SearchArgs& a, uint8_t* region, int64_t qi) {
+template <typename TX, typename TQ, int LP>
+__device__ __forceinline__ void init_search(WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, uint8_t* region, int64_t qi) {
   s.X = reinterpret_cast<const TX*>(a.X);
   s.d = a.d;
   s.lpr = a.lpr;
@@ -110,16 +118,16 @@ __device__ __forceinline__ void init_search(WarpSearch<TX, TQ>& s, const SearchA
   s.ever_mask = a.ever_size - 1u;
 }
 
-template <typename TX, typename TQ>
-__device__ __forceinline__ void zero_ever(WarpSearch<TX, TQ>& s, uint32_t size) {
+template <typename TX, typename TQ, int LP>
+__device__ __forceinline__ void zero_ever(WarpSearch<TX, TQ, LP>& s, uint32_t size) {
   if (!s.ever) return;
   for (uint32_t i = lane_id(); i < size; i += 32) s.ever[i] = 0u;
   __syncwarp();
   __threadfence_block();
 }
 
-template <typename TX, typename TQ>
-__device__ __forceinline__ void set_layer(WarpSearch<TX, TQ>& s, const LayerDev& L) {
+template <typename TX, typename TQ, int LP>
+__device__ __forceinline__ void set_layer(WarpSearch<TX, TQ, LP>& s, const LayerDev& L) {
   s.adj = L.adj;
   s.k = L.k;
   s.to_row = L.to_row;
@@ -127,8 +135,8 @@ __device__ __forceinline__ void set_layer(WarpSearch<TX, TQ>& s, const LayerDev&
 }
 
 // hits -> output rows; float keys optionally re-scored sequentially
-template <typename TX, typename TQ>
-__device__ void write_hits(const WarpSearch<TX, TQ>& s, const SearchArgs& a, int64_t qi, const int32_t* to_row,
+template <typename TX, typename TQ, int LP>
+__device__ void write_hits(const WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64_t qi, const int32_t* to_row,
                            int extra_visited, int extra_distinct) {
   using Key = typename VecTraits<TX, TQ>::Key;
   const int lane = lane_id();
@@ -161,15 +169,15 @@ __device__ void write_hits(const WarpSearch<TX, TQ>& s, const SearchArgs& a, int
 }
 
 // ------------------------------------------------------------------ query()
-template <typename TX, typename TQ>
-__global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ SearchArgs a) {
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   using Key = typename VecTraits<TX, TQ>::Key;
   const int wib = threadIdx.x >> 5;
   const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (qi >= a.m) return;
   const int lane = lane_id();
-  WarpSearch<TX, TQ> s;
+  WarpSearch<TX, TQ, LP> s;
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   set_layer(s, a.layer);
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ Sear
   const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
   Key bk;
   int bi;
-  warp_topk_scan<TX, TQ>(s.X, a.d, s.qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, s.crow, s.ckey, bk, bi);
+  warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, s.crow, s.ckey, bk, bi);
   int sid = -1;
   if (lane < kk) sid = a.top_rows ? __ldg(a.top_rows + bi) : bi;
   s.seed(bk, sid, kk);
@@ -190,15 +198,15 @@ __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ Sear
 }
 
 // ------------------------------------------------------------ greedy_search
-template <typename TX, typename TQ>
-__global__ void __launch_bounds__(256) greedy_kernel(const __grid_constant__ SearchArgs a) {
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   using Key = typename VecTraits<TX, TQ>::Key;
   const int wib = threadIdx.x >> 5;
   const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (qi >= a.m) return;
   const int lane = lane_id();
-  WarpSearch<TX, TQ> s;
+  WarpSearch<TX, TQ, LP> s;
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   set_layer(s, a.layer);
@@ -220,15 +228,15 @@ __global__ void __launch_bounds__(256) greedy_kernel(const __grid_constant__ Sea
 }
 
 // ------------------------------------------------------- hierarchical_query
-template <typename TX, typename TQ>
-__global__ void __launch_bounds__(256) descent_kernel(const __grid_constant__ SearchArgs a) {
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   using Key = typename VecTraits<TX, TQ>::Key;
   const int wib = threadIdx.x >> 5;
   const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (qi >= a.m) return;
   const int lane = lane_id();
-  WarpSearch<TX, TQ> s;
+  WarpSearch<TX, TQ, LP> s;
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   const LayerDev& Ls = a.layers[a.start];
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(256) descent_kernel(const __grid_constant__ Se
   const int kk = min(a.c.k_out, hi - lo);
   Key bk;
   int bi;
-  warp_topk_scan<TX, TQ>(s.X, a.d, s.qs, a.lpr, Ls.to_row, lo, hi, kk, s.crow, s.ckey, bk, bi);
+  warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, Ls.to_row, lo, hi, kk, s.crow, s.ckey, bk, bi);
   int id = lane < kk ? bi + lo : -1;
   int nh = kk;
   int visited = hi - lo, steps = 0, distinct = (hi - lo) - kk, forgotten = 0, term = TERM_EMPTY;
@@ -326,8 +334,8 @@ struct SymArgs {
   int32_t x_end;  // recheck only requests of nodes x < x_end
 };
 
-template <typename TX>
-__global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ SymArgs a) {
+template <typename TX, int LP>
+__global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(const __grid_constant__ SymArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   using Key = typename VecTraits<TX, TX>::Key;
   const int wib = threadIdx.x >> 5;
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
   const bool present = __any_sync(FULL, slot == x);
   int v = 0;
   int cand = -1;
-  WarpSearch<TX, TX> s;
+  WarpSearch<TX, TX, LP> s;
   if (!present) {
     s.X = reinterpret_cast<const TX*>(a.X);
     s.d = a.d;
@@ -430,7 +438,7 @@ __global__ void __launch_bounds__(256) symcheck_kernel(const __grid_constant__ S
 }
 
 // ----------------------------------------------------------- exhaustive_topk
-template <typename TX, typename TQ>
+template <typename TX, typename TQ, int LP>
 __global__ void __launch_bounds__(256) topk_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   using Key = typename VecTraits<TX, TQ>::Key;
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(256) topk_kernel(const __grid_constant__ Searc
   const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
   Key bk;
   int bi;
-  warp_topk_scan<TX, TQ>(reinterpret_cast<const TX*>(a.X), a.d, qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, crow,
+  warp_topk_scan<TX, TQ, LP>(reinterpret_cast<const TX*>(a.X), a.d, qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, crow,
                          ckey, bk, bi);
   const int k_out = a.c.k_out;
   if (lane < k_out) {
@@ -556,6 +564,29 @@ int launch_warps(Kern kern, const SearchArgs& a, int64_t items, size_t region, c
   return GGNN_OK;
 }
 
+// Launch the LP-specialised instantiation matching a.lpr (see warp_dists_t).
+#define GGNN_LAUNCH_LP(KER, TX, TQ, ...)                                          \
+  (a.lpr == 8    ? launch_warps(KER<TX, TQ, 8>, __VA_ARGS__)                     \
+   : a.lpr == 32 ? launch_warps(KER<TX, TQ, 32>, __VA_ARGS__)                    \
+                 : launch_warps(KER<TX, TQ, 0>, __VA_ARGS__))
+
+template <typename TX>
+int launch_sym(const SymArgs& a, int64_t items, cudaStream_t st) {
+  int W = pick_warps(a.region, SYM_THREADS / 32);
+  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
+  size_t smem = (size_t)W * a.region;
+  int64_t grid = (items + W - 1) / W;
+  auto go = [&](auto kern) -> int {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
+    GGNN_LAUNCH_CHECK();
+    return GGNN_OK;
+  };
+  if (a.lpr == 8) return go(symcheck_kernel<TX, 8>);
+  if (a.lpr == 32) return go(symcheck_kernel<TX, 32>);
+  return go(symcheck_kernel<TX, 0>);
+}
+
 int qelem_of(int dtype) { return dtype == GGNN_U8 ? 1 : 4; }
 
 int fill_common(SearchArgs& a, const ggnn_vectors* X, const ggnn_queries* Q, const ggnn_search_params* p) {
@@ -656,9 +687,9 @@ int ggnn_query_batch(const ggnn_vectors* X, const ggnn_layer* bottom, const int3
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return launch_warps(query_kernel<float, float>, a, a.m, a.region, st);
-    case 1: return launch_warps(query_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
-    default: return launch_warps(query_kernel<uint8_t, float>, a, a.m, a.region, st);
+    case 0: return GGNN_LAUNCH_LP(query_kernel, float, float, a, a.m, a.region, st);
+    case 1: return GGNN_LAUNCH_LP(query_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
+    default: return launch_warps(query_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
   }
 }
 
@@ -684,9 +715,9 @@ int ggnn_greedy_batch(const ggnn_vectors* X, const ggnn_layer* layer, const ggnn
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return launch_warps(greedy_kernel<float, float>, a, a.m, a.region, st);
-    case 1: return launch_warps(greedy_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
-    default: return launch_warps(greedy_kernel<uint8_t, float>, a, a.m, a.region, st);
+    case 0: return GGNN_LAUNCH_LP(greedy_kernel, float, float, a, a.m, a.region, st);
+    case 1: return GGNN_LAUNCH_LP(greedy_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
+    default: return launch_warps(greedy_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
   }
 }
 
@@ -716,9 +747,9 @@ int ggnn_descent_batch(const ggnn_vectors* X, const ggnn_layer* layers, int32_t 
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return launch_warps(descent_kernel<float, float>, a, a.m, a.region, st);
-    case 1: return launch_warps(descent_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
-    default: return launch_warps(descent_kernel<uint8_t, float>, a, a.m, a.region, st);
+    case 0: return GGNN_LAUNCH_LP(descent_kernel, float, float, a, a.m, a.region, st);
+    case 1: return GGNN_LAUNCH_LP(descent_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
+    default: return launch_warps(descent_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
   }
 }
 
@@ -747,8 +778,8 @@ int ggnn_merge_descent(const ggnn_vectors* X, const ggnn_layer* layers, int32_t 
   a.dists = d_dists;
   a.counters = d_counters;
   cudaStream_t st = as_stream(stream);
-  if (X->dtype == GGNN_F32) return launch_warps(descent_kernel<float, float>, a, a.m, a.region, st);
-  return launch_warps(descent_kernel<uint8_t, uint8_t>, a, a.m, a.region, st);
+  if (X->dtype == GGNN_F32) return GGNN_LAUNCH_LP(descent_kernel, float, float, a, a.m, a.region, st);
+  return GGNN_LAUNCH_LP(descent_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
 }
 
 int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const double* d_nnd,
@@ -781,20 +812,9 @@ int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const d
   a.req_cap = req_cap;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
   a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
-  int W = pick_warps(a.region, 8);
-  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
-  size_t smem = (size_t)W * a.region;
   cudaStream_t st = as_stream(stream);
-  int64_t grid = (npairs + W - 1) / W;
-  if (X->dtype == GGNN_U8) {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);
-  } else {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    symcheck_kernel<float><<<(unsigned)grid, W * 32, smem, st>>>(a);
-  }
-  GGNN_LAUNCH_CHECK();
-  return GGNN_OK;
+  if (X->dtype == GGNN_U8) return launch_sym<uint8_t>(a, npairs, st);
+  return launch_sym<float>(a, npairs, st);
 }
 
 int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_req, int64_t nreq,
@@ -821,20 +841,9 @@ int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_
   a.x_end = x_end;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
   a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
-  int W = pick_warps(a.region, 8);
-  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
-  size_t smem = (size_t)W * a.region;
   cudaStream_t st = as_stream(stream);
-  int64_t grid = (nreq + W - 1) / W;
-  if (X->dtype == GGNN_U8) {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);
-  } else {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    symcheck_kernel<float><<<(unsigned)grid, W * 32, smem, st>>>(a);
-  }
-  GGNN_LAUNCH_CHECK();
-  return GGNN_OK;
+  if (X->dtype == GGNN_U8) return launch_sym<uint8_t>(a, nreq, st);
+  return launch_sym<float>(a, nreq, st);
 }
 
 int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const int32_t* d_x, const int32_t* d_z,
@@ -863,20 +872,9 @@ int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const i
   a.fallback = d_fallback;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
   a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
-  int W = pick_warps(a.region, 8);
-  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
-  size_t smem = (size_t)W * a.region;
   cudaStream_t st = as_stream(stream);
-  int64_t grid = (npairs + W - 1) / W;
-  if (X->dtype == GGNN_U8) {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    symcheck_kernel<uint8_t><<<(unsigned)grid, W * 32, smem, st>>>(a);
-  } else {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(symcheck_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    symcheck_kernel<float><<<(unsigned)grid, W * 32, smem, st>>>(a);
-  }
-  GGNN_LAUNCH_CHECK();
-  return GGNN_OK;
+  if (X->dtype == GGNN_U8) return launch_sym<uint8_t>(a, npairs, st);
+  return launch_sym<float>(a, npairs, st);
 }
 
 int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t nrows, const ggnn_queries* Q,
@@ -895,9 +893,9 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   a.region = 128 + align16(32 * (size_t)keysize) + align16((size_t)X->d * qelem_of(qd));
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return launch_warps(topk_kernel<float, float>, a, a.m, a.region, st, 8);
-    case 1: return launch_warps(topk_kernel<uint8_t, uint8_t>, a, a.m, a.region, st, 8);
-    default: return launch_warps(topk_kernel<uint8_t, float>, a, a.m, a.region, st, 8);
+    case 0: return GGNN_LAUNCH_LP(topk_kernel, float, float, a, a.m, a.region, st, 8);
+    case 1: return GGNN_LAUNCH_LP(topk_kernel, uint8_t, uint8_t, a, a.m, a.region, st, 8);
+    default: return launch_warps(topk_kernel<uint8_t, float, 0>, a, a.m, a.region, st, 8);
   }
 }
 

@@ -53,14 +53,17 @@ inline size_t warp_region_bytes(int cap, int vsz, int hlog, int64_t d, int qelem
   return b;
 }
 
+// Refcount table size: at most cap + vsz ids are live at once (ring u visited
+// ring); the table keeps >= 64 + cap / 8 spare slots beyond that so probing
+// always meets an empty slot (tombstones are purged by rebuild(), see merge()).
 inline int table_log2(int cap, int vsz) {
-  int need = 2 * (cap + vsz);
+  int need = cap + vsz + 64 + cap / 8;
   int lg = 6;
   while ((1 << lg) < need) ++lg;
   return lg;
 }
 
-template <typename TX, typename TQ>
+template <typename TX, typename TQ, int LP = 0>
 struct WarpSearch {
   using Key = typename VecTraits<TX, TQ>::Key;
   using KO = KeyOps<Key>;
@@ -91,7 +94,7 @@ struct WarpSearch {
   uint32_t* ever;
   uint32_t ever_mask;
   // warp-uniform state
-  int L, vlen, vpos, used;
+  int L, vlen, vpos, used, rebuild_at;
   int visited, steps, distinct, forgotten, term;
   bool found_target;
 
@@ -121,6 +124,7 @@ struct WarpSearch {
   __device__ void reset() {
     ht.clear();
     L = vlen = vpos = used = 0;
+    rebuild_at = (int)((ht.mask + 1) * 3 / 4);
     visited = steps = distinct = forgotten = 0;
     term = TERM_EMPTY;
     found_target = false;
@@ -156,6 +160,10 @@ struct WarpSearch {
     for (int i = lane; i < L; i += 32) u += ht.add_one((uint32_t)rid[i]);
     for (int i = lane; i < vlen; i += 32) u += ht.add_one((uint32_t)vring[i]);
     used = warp_sum(u);
+    // next purge once tombstones fill an eighth of the table, never so late
+    // that fewer than 40 slots stay empty (one merge adds at most 32)
+    const int size = (int)ht.mask + 1;
+    rebuild_at = min(max(size * 3 / 4, used + size / 8), size - 40);
     __syncwarp();
   }
 
@@ -262,7 +270,7 @@ struct WarpSearch {
     used += warp_sum(took);
     L = newL;
     __syncwarp();
-    if (used > (int)((ht.mask + 1) >> 1)) rebuild();
+    if (used > rebuild_at) rebuild();
   }
 
   // Seeds: lanes [0, n) hold (key, id) in the caller's order; duplicates and
@@ -326,7 +334,7 @@ struct WarpSearch {
         cid[ci] = nb;
       }
       __syncwarp();
-      warp_dists<TX, TQ>(X, d, qs, crow, nc, ckey, lpr);
+      warp_dists_t<TX, TQ, LP>(X, d, qs, crow, nc, ckey, lpr);
       __syncwarp();
       Key key = KO::max_key();
       int id = INT_MAX;
@@ -408,7 +416,7 @@ __device__ __forceinline__ void topk_merge_chunk(Key& bk, int& bi, Key ck, int c
 // Exhaustive top-kk (kk <= 32) over rows[lo..hi) (or the index range itself
 // when rows is null), ties by local index; the result sits in lanes [0, kk)
 // as (key, local index) -- the reference's exhaustive_topk (_core.pyx:86-104).
-template <typename TX, typename TQ>
+template <typename TX, typename TQ, int LP = 0>
 __device__ void warp_topk_scan(const TX* X, int64_t d, const TQ* qs, int lpr, const int32_t* rows, int lo, int hi,
                                int kk, int* crow, typename VecTraits<TX, TQ>::Key* ckey,
                                typename VecTraits<TX, TQ>::Key& bk, int& bi) {
@@ -421,7 +429,7 @@ __device__ void warp_topk_scan(const TX* X, int64_t d, const TQ* qs, int lpr, co
     const int cnt = min(32, hi - base);
     if (lane < cnt) crow[lane] = rows ? __ldg(rows + base + lane) : base + lane;
     __syncwarp();
-    warp_dists<TX, TQ>(X, d, qs, crow, cnt, ckey, lpr);
+    warp_dists_t<TX, TQ, LP>(X, d, qs, crow, cnt, ckey, lpr);
     __syncwarp();
     Key ck = KO::max_key();
     int cx = INT_MAX;
