@@ -43,10 +43,16 @@ constexpr int MAX_LAYERS = 24;
 // registers at 80 per thread, so 24 searches share an SM (shared memory
 // allows about as many for the default 266-entry ring + 512-entry visited
 // ring + 1024-slot table).  Sym-check CTAs run 8 warps of small searches.
+#ifndef GGNN_SEARCH_MIN_BLOCKS
+#define GGNN_SEARCH_MIN_BLOCKS 7
+#endif
 constexpr int SEARCH_THREADS = 128;
-constexpr int SEARCH_MIN_BLOCKS = 6;
+constexpr int SEARCH_MIN_BLOCKS = GGNN_SEARCH_MIN_BLOCKS;
 constexpr int SYM_THREADS = 256;
-constexpr int SYM_MIN_BLOCKS = 3;
+#ifndef GGNN_SYM_MIN_BLOCKS
+#define GGNN_SYM_MIN_BLOCKS 4
+#endif
+constexpr int SYM_MIN_BLOCKS = GGNN_SYM_MIN_BLOCKS;
 
 struct LayerDev {
   const int32_t* adj;
@@ -178,6 +184,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kerne
   if (qi >= a.m) return;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
+  VRING_DECL(s);
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   set_layer(s, a.layer);
@@ -207,6 +214,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kern
   if (qi >= a.m) return;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
+  VRING_DECL(s);
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   set_layer(s, a.layer);
@@ -237,6 +245,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_ker
   if (qi >= a.m) return;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
+  VRING_DECL(s);
   init_search(s, a, smem + (size_t)wib * a.region, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   const LayerDev& Ls = a.layers[a.start];
@@ -380,6 +389,7 @@ __global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(c
   int v = 0;
   int cand = -1;
   WarpSearch<TX, TX, LP> s;
+  VRING_DECL(s);
   if (!present) {
     s.X = reinterpret_cast<const TX*>(a.X);
     s.d = a.d;

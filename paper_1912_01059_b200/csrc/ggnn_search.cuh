@@ -40,13 +40,29 @@ constexpr int FLAG_EXACT_DISTS = 2;  // re-score returned hits sequentially (bit
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Visited rings of up to 32 * VR_SLOTS entries live in per-lane local memory
+// (entry i in lane i & 31, slot i >> 5): the ring is written once per
+// expansion and read back only when it wraps, so it needs no shared memory.
+#ifndef GGNN_VR_SLOTS
+#define GGNN_VR_SLOTS 16
+#endif
+constexpr int VR_SLOTS = GGNN_VR_SLOTS;
+__host__ __device__ inline bool vring_local(int vsz) { return vsz <= 32 * VR_SLOTS; }
+
+// Each search kernel declares its lane's slice of the visited ring outside the
+// WarpSearch object (an indexed array member would push the whole object --
+// counters included -- to the stack):  VRING_DECL(s);
+#define VRING_DECL(s)                      \
+  int vring_lane_[VR_SLOTS > 0 ? VR_SLOTS : 1]; \
+  (s).vr = vring_lane_
+
 // Byte size of one warp's shared region.
 inline size_t warp_region_bytes(int cap, int vsz, int hlog, int64_t d, int qelem, int keysize) {
   size_t b = 0;
   b += align16((size_t)cap * keysize);      // rk
   b += align16((size_t)cap * 4);            // rid
   b += align16((size_t)((cap + 127) / 128) * 128);  // rvis (padded for 4-byte scans)
-  b += align16((size_t)vsz * 4);            // vring
+  if (!vring_local(vsz)) b += align16((size_t)vsz * 4);  // vring (shared only when large)
   b += align16((size_t)(1u << hlog) * 4);   // ht
   b += 32 * 4 + 32 * 4 + align16(32 * (size_t)keysize);  // crow, cid, ckey
   b += align16((size_t)d * qelem);          // qs
@@ -85,7 +101,8 @@ struct WarpSearch {
   Key* rk;
   int* rid;
   uint8_t* rvis;
-  int* vring;
+  int* vring;  // shared visited ring (vsz > 32 * VR_SLOTS only)
+  int* vr;  // local visited ring (the kernel's per-lane array, see VRING_DECL)
   RefTable ht;
   int* crow;
   int* cid;
@@ -106,8 +123,11 @@ struct WarpSearch {
     p += align16((size_t)c.cap * 4);
     rvis = p;
     p += align16((size_t)((c.cap + 127) / 128) * 128);
-    vring = reinterpret_cast<int*>(p);
-    p += align16((size_t)c.vsz * 4);
+    vring = nullptr;
+    if (!vring_local(c.vsz)) {
+      vring = reinterpret_cast<int*>(p);
+      p += align16((size_t)c.vsz * 4);
+    }
     ht.t = reinterpret_cast<uint32_t*>(p);
     ht.mask = (1u << c.hlog) - 1u;
     ht.shift = 32 - c.hlog;
@@ -158,7 +178,7 @@ struct WarpSearch {
     ht.clear();
     int u = 0;
     for (int i = lane; i < L; i += 32) u += ht.add_one((uint32_t)rid[i]);
-    for (int i = lane; i < vlen; i += 32) u += ht.add_one((uint32_t)vring[i]);
+    for (int i = lane; i < vlen; i += 32) u += ht.add_one((uint32_t)(vring ? vring[i] : vr[i >> 5]));
     used = warp_sum(u);
     // next purge once tombstones fill an eighth of the table, never so late
     // that fewer than 40 slots stay empty (one merge adds at most 32)
@@ -189,12 +209,27 @@ struct WarpSearch {
   __device__ void vring_push(int node) {
     const int lane = lane_id();
     if (vlen == c.vsz) {
-      int old = vring[vpos];
+      int old;
+      if (vring) {
+        old = vring[vpos];
+        __syncwarp();
+        if (lane == 0) vring[vpos] = node;
+      } else {
+        int o = 0;
+        if (lane == (vpos & 31)) {
+          o = vr[vpos >> 5];
+          vr[vpos >> 5] = node;
+        }
+        old = __shfl_sync(FULL, o, vpos & 31);
+      }
       if (ht.dec((uint32_t)old)) forgotten++;
-      if (lane == 0) vring[vpos] = node;
       vpos = (vpos + 1 == c.vsz) ? 0 : vpos + 1;
     } else {
-      if (lane == 0) vring[vlen] = node;
+      if (vring) {
+        if (lane == 0) vring[vlen] = node;
+      } else if (lane == (vlen & 31)) {
+        vr[vlen >> 5] = node;
+      }
       vlen++;
     }
     __syncwarp();
