@@ -61,12 +61,19 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(self.local)
+        # GGNN_DIST_BACKEND=gloo lets several ranks share one GPU (functional
+        # tests of the sharded path on a 1-GPU box); the product path is NCCL
+        self.backend = os.environ.get("GGNN_DIST_BACKEND", "nccl")
+        self.device = self.local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(self.device)
         self.on = self.world > 1
         if self.on:
             import torch.distributed as dist
 
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                dist.init_process_group(self.backend)
             self.dist = dist
 
     def barrier(self):
@@ -76,7 +83,7 @@ class Dist:
     def max(self, v: float) -> float:
         if not self.on:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda" if self.backend == "nccl" else "cpu")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -274,6 +281,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, dist, ga)
+    if dist.world > 1:
+        return run_sharded(args, dist, ga, torch)
 
     base, Q = make_workload(args)
     ds = ga.Dataset(base)
@@ -336,8 +345,7 @@ def main():
     kk = dh.layers[0].k
     bytes_per_launch = int((c[:, 0] * d * e + c[:, 1] * (4 * kk + 4) + d * e + 8 * 10).sum())
     avg_launch = float(np.mean(per_launch))
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak, peak_src = _peak()
     achieved = bytes_per_launch / avg_launch / 1e9
     traffic = None
     prof = ROOT / "profiles" / "query_kernel_ncu.json"
@@ -394,7 +402,7 @@ def main():
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel_ms": avg_launch * 1e3, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"},
+                     "kernel_ms": avg_launch * 1e3, "peak_source": peak_src},
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
@@ -403,6 +411,152 @@ def main():
         print(s, flush=True)
         if args.out:
             Path(args.out).write_text(s + "\n")
+    dist.close()
+
+
+def _peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        return float(json.loads(f.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    return 6650.0, "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def _bytes_per_launch(cnt, d, e, k, k_out):
+    c = cnt.astype(np.int64)
+    return int((c[:, 0] * d * e + c[:, 1] * (4 * k + 4) + d * e + 8 * k_out).sum())
+
+
+def run_sharded(args, dist, ga, torch):
+    """N > 1: one 1M-point shard per GPU of an N-million-point latent16 index
+    (shard 0 = the C2 data), the 10k-query batch replicated on every rank,
+    each step = search (query kernel into the shard block) + id globalization
+    + NCCL all-gather + GPU G-way merge.  Weak scaling: per-GPU work is fixed
+    (m queries on one 1M shard); value counts shard-queries (N * m per step)."""
+    from paper_1912_01059_b200 import _native as N
+    from paper_1912_01059_b200.device import device_hierarchy
+    from paper_1912_01059_b200.distributed import ShardGroup
+    from paper_1912_01059_b200.shard import block_layout, block_pointers
+    from paper_1912_01059_b200.synthetic import make_latent16, make_latent16_shard
+
+    G, r = dist.world, dist.rank
+    _, Q = make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234)
+    base = make_latent16_shard(n=args.n, d=args.d, shard=r, seed=1234)
+    ds = ga.Dataset(base)
+    dist.barrier()
+    h, bstats = ga.build(ds, ga.BuildConfig(seed=7))
+    build_s = dist.max(bstats.build_seconds)
+    grp = ShardGroup(h, np.arange(r * args.n, (r + 1) * args.n, dtype=np.int32))
+    gt_ids, _ = grp.exact_arrays(Q, 10)
+    sweep, chosen = [], None
+    for tau in ([args.tau] if args.tau is not None else TAUS):
+        res = grp.query_arrays(Q, ga.QueryConfig(k_out=10, tau=tau))
+        row = {"tau": tau, "R@1": recall_at(res.ids, gt_ids[:, 0], 1), "R@10": recall_at(res.ids, gt_ids[:, 0], 10),
+               "kR@10": k_recall_at(res.ids, gt_ids, 10), "V": float(res.counters[:, 0].mean()) / G,
+               "T": float(res.counters[:, 1].mean()) / G}
+        sweep.append(row)
+        if row["R@10"] >= 0.99:
+            chosen = row
+            break
+    chosen = chosen or sweep[-1]
+    tau = chosen["tau"]
+    qcfg = ga.QueryConfig(k_out=10, tau=tau)
+
+    dh = device_hierarchy(h)
+    dv = dh.vectors
+    dq, qs = dv.queries(Q)
+    m = Q.shape[0]
+    bb = block_layout(m, 10)[0]
+    send = N.empty((bb,), torch.uint8)
+    recv = N.empty((G * bb,), torch.uint8)
+    ids_p, dists_p, cnt_p = block_pointers(send, 0, m, 10)
+    out_ids = N.empty((m, 10), torch.int32)
+    out_d = N.empty((m, 10), torch.float64)
+    out_c = N.empty((m, 5), torch.int32)
+    params = N.search_params(10, qcfg.prioq_size, qcfg.visited_size, tau, qcfg.max_iterations, 0)
+    gid = grp.gid_dev()
+    stream = torch.cuda.current_stream()
+    qev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+
+    def step(i=None):
+        if i is not None:
+            qev[2 * i].record(stream)
+        N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
+               N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, ids_p, dists_p,
+               cnt_p, None, 0, N.stream_ptr())
+        if i is not None:
+            qev[2 * i + 1].record(stream)
+        N.call("ggnn_shard_globalize", ids_p, m * 10, N.ptr(gid), args.n, N.stream_ptr())
+        grp.exchange(send, recv)
+        N.call("ggnn_shard_merge", N.ptr(recv), G, m, 10, 10, N.ptr(out_ids), N.ptr(out_d), N.ptr(out_c),
+               N.stream_ptr())
+
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        clocks.wait_first()
+        # warm-up: a FIXED count on every rank (each step is a collective)
+        for w in range(max(args.warmup, 16)):
+            step()
+            if w % 8 == 7:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(args.steps):
+            step(i)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    t_max = dist.max(evs[0].elapsed_time(evs[-1]) / 1e3)
+    value = G * m * args.steps / t_max
+    kern = float(np.mean([qev[2 * i].elapsed_time(qev[2 * i + 1]) for i in range(args.steps)])) / 1e3
+    coff = block_layout(m, 10)[2]
+    own = send[coff:coff + m * 20].view(torch.int32).view(m, 5).cpu().numpy()  # this rank's V, T counters
+    e = 1 if dv.exact_integers else 4
+    bpl = _bytes_per_launch(own, args.d, e, dh.layers[0].k, 10)
+    peak, peak_src = _peak()
+    achieved = bpl / kern / 1e9
+
+    Q_host = np.ascontiguousarray(Q, dtype=np.float32)
+    for _ in range(max(1, args.warmup)):
+        grp.query_arrays(Q_host, qcfg)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = grp.query_arrays(Q_host, qcfg)
+    torch.cuda.synchronize()
+    e2e_t = dist.max(time.perf_counter() - t0)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8" if dv.exact_integers else "f32",
+        "data": "synthetic latent16 (SURVEY.md 8d G_B), seed 1234; shard r>0 from stream (1234, 0x5AD, r)",
+        "config": {"workload": f"sharded latent16 {G}x{args.n}x{args.d} (one SIFT1M-shaped shard per GPU), "
+                               f"{m} replicated queries, k=10, k_build=24",
+                   "units": "shard-queries: each step searches all m queries on each of the N shards, then "
+                            "all-gathers and merges the per-shard top-10 (value = N*m*steps/t)",
+                   "tau": tau, "recall_merged": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
+                   "mean_visited_per_shard": chosen["V"], "mean_steps_per_shard": chosen["T"], "tau_sweep": sweep,
+                   "build_seconds_max_over_ranks": build_s,
+                   "parallelism": f"sharded x{G}: NCCL all_gather_into_tensor of {bb} B/rank + ggnn_shard_merge",
+                   "l2": "inputs larger than L2 (u8 shard 128 MB + adjacency 96 MB per GPU)"},
+        "build_seconds": build_s,
+        "e2e": {"value": G * m * args.steps / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(m * args.d * e),
+                "d2h_bytes_per_step": int(out.ids.nbytes + out.dists.nbytes + out.counters.nbytes),
+                "api": "ShardGroup.query_arrays(numpy queries) -> host arrays (every rank)"},
+        "gpu_launches": 3 * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": bpl, "kernel_ms": kern * 1e3,
+                     "kernel": "query_kernel (rank 0)", "peak_source": peak_src},
+        "clocks": clocks.summary(),
+        "cpu_baseline": None,
+    }
+    if dist.rank == 0:
+        js = json.dumps(line)
+        print(js, flush=True)
+        if args.out:
+            Path(args.out).write_text(js + "\n")
     dist.close()
 
 

@@ -91,7 +91,44 @@ class ShardGroup:
         return merge_blocks(recv, self.world, m, cfg.k_out, cfg.k_out)
 
     def exchange(self, send, recv) -> None:
+        """All-gather of the shard blocks (NCCL on device buffers; a gloo
+        group -- CPU tests, several ranks sharing one GPU -- stages through
+        host memory)."""
+        if recv.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            r = recv.cpu()
+            self.dist.all_gather_into_tensor(r, send.cpu(), group=self.group)
+            recv.copy_(r)
+            return
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
+
+    def exact_arrays(self, queries: np.ndarray, k: int, out: str = "numpy"):
+        """Exact global top-k (k <= 32) of a replicated batch: every rank
+        scans its shard (ggnn_exhaustive_topk) into its block, then the same
+        all-gather + merge as a search (ground truth for sharded recall)."""
+        from .device import DeviceVectors
+        from .shard import block_pointers
+
+        Q = np.ascontiguousarray(queries, dtype=np.float32)
+        m = Q.shape[0]
+        bb = self.block_bytes(m, k)
+        send = self.new_buffer(bb)
+        send.zero_()
+        recv = self.new_buffer(self.world * bb)
+        dv = DeviceVectors.of(self.h.dataset)
+        dq, qs = dv.queries(Q)
+        ids_p, dists_p, _ = block_pointers(send, 0, m, k)
+        N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), ids_p,
+               dists_p, N.stream_ptr())
+        N.call("ggnn_shard_globalize", ids_p, m * k, N.ptr(self.gid_dev()), int(self.gid_host.shape[0]),
+               N.stream_ptr())
+        self.exchange(send, recv)
+        from .shard import merge_blocks
+
+        ids, dists, cnt = merge_blocks(recv, self.world, m, k, k)
+        del dq
+        if out == "device":
+            return ids, dists
+        return np.asarray(ids.cpu()), np.asarray(dists.cpu())
 
     def query_arrays(self, queries: np.ndarray, cfg: QueryConfig | None = None, out: str = "numpy"):
         """Sharded query of a replicated batch; every rank returns the merged

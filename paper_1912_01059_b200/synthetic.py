@@ -62,3 +62,20 @@ def make_latent16(n=10000, d=128, m=1000, seed=1234, as_float=False):
     rngq = np.random.default_rng((seed, 0x51E7))
     queries = _latent_draw(rngq, A, C, m, d, as_float)
     return base, queries
+
+
+def make_latent16_shard(n=1_000_000, d=128, shard=0, seed=1234, as_float=False):
+    """Base rows of shard `shard` of a multi-million-point latent16 index
+    (bench.py --gpus N): shard 0 is exactly make_latent16(n, d)'s base (the
+    C2 data), shard s > 0 draws n further rows of the same distribution (the
+    shared (A, C) of `seed`) from the stream (seed, 0x5AD, s)."""
+    if shard == 0:
+        return make_latent16(n=n, d=d, m=1, seed=seed, as_float=as_float)[0]
+    rng0 = np.random.default_rng(seed)
+    A = rng0.standard_normal((16, d)) / 4.0
+    C = rng0.standard_normal((64, 16)) * 2.0
+    out = np.empty((n, d), dtype=np.float32)
+    for c, lo in enumerate(range(0, n, CHUNK)):
+        hi = min(n, lo + CHUNK)
+        out[lo:hi] = _latent_draw(np.random.default_rng((seed, 0x5AD, shard, c)), A, C, hi - lo, d, as_float)
+    return out

@@ -140,3 +140,60 @@ def test_brute_force_oracle_and_knn_graph():
     for i in range(0, 700, 37):
         ids, _ = O.exhaustive_topk(X, X[i], 4)
         np.testing.assert_array_equal(kg[i], [v for v in ids if v != i][:3])
+
+
+def _group_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1912_01059_b200.distributed import ShardGroup
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # ranks share the one GPU
+    try:
+        base, Q = make_latent16(n=3000, d=32, m=150, seed=3)
+        grp = ShardGroup.from_dataset(ga.Dataset(base), ga.BuildConfig(seed=7))
+        res = grp.query_arrays(Q, ga.QueryConfig(k_out=10, tau=0.6))
+        gt_ids, gt_d = grp.exact_arrays(Q, 10)
+        q.put((rank, res.ids, res.dists, res.counters, gt_ids, gt_d))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_group_real_kernels_two_ranks():
+    """ShardGroup with the real kernels (2 ranks on one GPU, gloo exchange):
+    equals query_sharded_arrays over the same shards built in one process,
+    and its exact path equals the single-index brute force."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_group_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    base, Q = make_latent16(n=3000, d=32, m=150, seed=3)
+    ds = ga.Dataset(base)
+    si, _ = ga.build_sharded(ds, 1500, ga.BuildConfig(seed=7))
+    ref = ga.query_sharded_arrays(si, Q, ga.QueryConfig(k_out=10, tau=0.6))
+    gt = ga.brute_force_oracle(ds, Q, 10)
+    for _, ids, dists, cnt, gi, gd in out:
+        np.testing.assert_array_equal(ids, ref.ids)
+        np.testing.assert_array_equal(dists, ref.dists)
+        np.testing.assert_array_equal(cnt, ref.counters)
+        np.testing.assert_array_equal(gi, gt.ids)
+        np.testing.assert_array_equal(gd, gt.dists)
