@@ -26,6 +26,18 @@ int ggnn_leaf_knn(const ggnn_vectors *X, const int32_t *d_nodes, const int32_t *
                   int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t *d_pos, double *d_dist, int32_t *d_adj,
                   int32_t k, double *d_nnd, double *d_dnn1, int32_t *d_reduced, void *stream);
 
+/* Same contract as ggnn_leaf_knn, forced onto the tcgen05 tensor-core path
+ * (kind::i8 MMA of the staged batch against itself, exact integer distances);
+ * GGNN_E_INVALID unless X is uint8 with d % 32 == 0, d <= 512 and every batch
+ * has 2..128 rows.  ggnn_leaf_knn takes this path automatically when eligible. */
+int ggnn_leaf_knn_tc(const ggnn_vectors *X, const int32_t *d_nodes, const int32_t *d_rows, const int64_t *d_offsets,
+                     int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t *d_pos, double *d_dist,
+                     int32_t *d_adj, int32_t k, double *d_nnd, double *d_dnn1, int32_t *d_reduced, void *stream);
+
+/* Number of tensor-core tiles whose MMA completion wait timed out since the
+ * library was loaded (0 in a healthy run; synchronizes). */
+int ggnn_tc_timeouts(void);
+
 /* Replaces: the per-node hierarchical_query calls of merge_layer
  * (build.py:146-197, search.py:140-210) for all m nodes of layer `stop` at
  * once.  Query i is base row d_query_rows[i]; it brute-forces the segment

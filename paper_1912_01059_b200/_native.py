@@ -66,6 +66,8 @@ _SIGS = {
     "ggnn_squared_l2_many": [P, P, P, I32, P, P],
     "ggnn_f32_to_u8": [P, I64, P, P, P],
     "ggnn_leaf_knn": [P, P, P, P, I64, I64, I32, P, P, P, I32, P, P, P, P],
+    "ggnn_leaf_knn_tc": [P, P, P, P, I64, I64, I32, P, P, P, I32, P, P, P, P],
+    "ggnn_tc_timeouts": [],
     "ggnn_merge_descent": [P, P, I32, I32, I32, P, I64, P, I32, I32, P, P, P, P, P],
     "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_sym_check_layer": [P, P, P, P, P, I32, F64, F64, I32, I32, I32, I32, I32, P, P, I64, P],

@@ -9,6 +9,7 @@
 #include "ggnn_build.h"
 #include "ggnn_capi_util.cuh"
 #include "ggnn_search.cuh"
+#include "ggnn_tc.cuh"
 
 namespace ggnn {
 
@@ -129,6 +130,143 @@ __global__ void __launch_bounds__(256) leaf_knn_kernel(const __grid_constant__ L
     }
     if (a.dnn1 && lane == 0) a.dnn1[a.nodes[gi]] = k_eff > 0 ? bk : KeyOps<double>::max_key();
   }
+}
+
+// ------------------------------------------------- leaf kNN on tcgen05 (u8)
+// One CTA (4 warps) per batch of m <= 128 uint8 rows.  The rows are staged in
+// shared memory in the interleaved K-major layout (ggnn_tc.cuh) and serve as
+// both operands of D = X X^T: d/32 tcgen05.mma kind::i8 instructions
+// (M = 128, N = m rounded up to 16, s32 accumulators in 128 TMEM columns),
+// issued by one thread and committed to an mbarrier.  Each thread then owns
+// one row (TMEM lane), reads its dot products with tcgen05.ld and forms exact
+// squared distances n_i + n_j - 2 d_ij (integers, the reference's _sqdist
+// values); every warp selects the k_nn smallest (distance, position) of its
+// 32 rows with the same bitonic top-k as the SIMT kernel -- batch_bruteforce
+// (_core.pyx:107-130) bit for bit.
+constexpr int TC_ROWS = 128;
+constexpr int TC_DSTRIDE = TC_ROWS + 1;
+__device__ int g_tc_timeouts = 0;
+
+inline size_t leaf_tc_smem(int64_t d) {
+  return (size_t)TC_ROWS * d + TC_ROWS * 4 + (size_t)TC_ROWS * TC_DSTRIDE * 4 + 16;
+}
+
+__global__ void __launch_bounds__(128, 1) leaf_knn_tc_kernel(const __grid_constant__ LeafArgs a, int64_t nbatches) {
+  extern __shared__ __align__(16) uint8_t smem_tc[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = (int)a.d;
+  uint8_t* A = smem_tc;
+  uint32_t* nrm = reinterpret_cast<uint32_t*>(smem_tc + (size_t)TC_ROWS * K);
+  uint32_t* D = nrm + TC_ROWS;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(D + TC_ROWS * TC_DSTRIDE);
+  uint32_t* taddr = reinterpret_cast<uint32_t*>(mbar + 1);
+  if (warp == 0) tc::tmem_alloc<128>(taddr);
+  if (tid == 0) tc::mbar_init(mbar, 1);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *taddr;
+  const uint8_t* X = reinterpret_cast<const uint8_t*>(a.X);
+  const int nch = K >> 4;
+  uint32_t phase = 0;
+  // persistent: TMEM and the mbarrier are set up once per CTA
+  for (int64_t b = blockIdx.x; b < nbatches; b += gridDim.x, phase ^= 1u) {
+    const int64_t off = a.offsets[b];
+    const int m = (int)(a.offsets[b + 1] - off);
+    const int n_pad = max(16, (m + 15) & ~15);
+    for (int t = tid; t < n_pad * nch; t += blockDim.x) {
+      const int r = t / nch, c = t - r * nch;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (r < m) {
+        const int32_t node = a.nodes[off + r];
+        const int32_t row = a.rows ? a.rows[off + r] : node;
+        v = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)row * K) + c);
+      }
+      *reinterpret_cast<uint4*>(A + tc::il_offset(r, c * 16, K)) = v;
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t idesc = tc::idesc_u8(TC_ROWS, n_pad);
+      const uint32_t base = tc::smem_u32(A);
+      const uint32_t sbo = (uint32_t)nch * 128u;
+      for (int s = 0; s < (K >> 5); ++s) {
+        const uint64_t dsc = tc::smem_desc(base + (uint32_t)s * 256u, 128u, sbo);
+        tc::mma_u8(tmem, dsc, dsc, idesc, s > 0 ? 1u : 0u);
+      }
+      tc::commit(mbar);
+    }
+    __syncwarp();
+    // squared norms while the tensor core works (reads the staged rows only)
+    if (tid < m) {
+      uint32_t sq = 0;
+      for (int c = 0; c < nch; ++c) {
+        const uint4 v = *reinterpret_cast<const uint4*>(A + tc::il_offset(tid, c * 16, K));
+        sq = __dp4a(v.x, v.x, sq);
+        sq = __dp4a(v.y, v.y, sq);
+        sq = __dp4a(v.z, v.z, sq);
+        sq = __dp4a(v.w, v.w, sq);
+      }
+      nrm[tid] = sq;
+    }
+    __syncthreads();
+    const bool ok = tc::mbar_wait(mbar, phase);
+    tc::fence_after_sync();
+    if (!ok && lane == 0) atomicAdd(&g_tc_timeouts, 1);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t ni = tid < m ? nrm[tid] : 0u;
+    for (int c0 = 0; c0 < n_pad; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + lane_base + (uint32_t)c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = c0 + j;
+        if (tid < m && col < m) D[tid * TC_DSTRIDE + col] = ni + nrm[col] - 2u * v[j];
+      }
+    }
+    __syncwarp();
+    const int k_eff = min(a.k_nn, m - 1);
+    if (k_eff < a.k_nn && tid == 0 && a.reduced) atomicAdd(a.reduced, 1);
+    for (int i = warp * 32; i < min(m, warp * 32 + 32); ++i) {
+      uint32_t bk = KeyOps<uint32_t>::max_key();
+      int bi = INT_MAX;
+      if (k_eff > 0) {
+        for (int jb = 0; jb < m; jb += 32) {
+          const int j = jb + lane;
+          uint32_t dv = KeyOps<uint32_t>::max_key();
+          int jj = INT_MAX;
+          if (j < m && j != i) {
+            dv = D[i * TC_DSTRIDE + j];
+            jj = j;
+          }
+          topk_merge_chunk(bk, bi, dv, jj, k_eff);
+        }
+      }
+      const int64_t gi = off + i;
+      const double bkd = (double)bk;
+      if (lane < a.k_nn) {
+        const bool v = lane < k_eff;
+        if (a.pos) a.pos[gi * a.k_nn + lane] = v ? bi : -1;
+        if (a.dist) a.dist[gi * a.k_nn + lane] = v ? bkd : KeyOps<double>::max_key();
+        if (a.adj && v) {
+          const int32_t node = a.nodes[gi];
+          a.adj[(int64_t)node * a.k + lane] = a.nodes[off + bi];
+          a.nnd[(int64_t)node * a.k_nn + lane] = bkd;
+        }
+      }
+      if (a.dnn1 && lane == 0) a.dnn1[a.nodes[gi]] = k_eff > 0 ? bkd : KeyOps<double>::max_key();
+    }
+    // the next batch overwrites the staged rows and TMEM: everyone must be done
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
+  if (warp == 0) tc::tmem_free<128>(tmem);
+}
+
+bool leaf_tc_eligible(const ggnn_vectors* X, int64_t max_batch) {
+  return X->dtype == GGNN_U8 && max_batch >= 2 && max_batch <= TC_ROWS && X->d % 32 == 0 && X->d <= 512 &&
+         (reinterpret_cast<uintptr_t>(X->d_data) & 15) == 0;
 }
 
 // ------------------------------------------------------------- merge rows
@@ -384,9 +522,10 @@ using namespace ggnn;
 
 extern "C" {
 
-int ggnn_leaf_knn(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* d_rows, const int64_t* d_offsets,
-                  int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t* d_pos, double* d_dist, int32_t* d_adj,
-                  int32_t k, double* d_nnd, double* d_dnn1, int32_t* d_reduced, void* stream) {
+static int leaf_knn_impl(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* d_rows,
+                         const int64_t* d_offsets, int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t* d_pos,
+                         double* d_dist, int32_t* d_adj, int32_t k, double* d_nnd, double* d_dnn1, int32_t* d_reduced,
+                         void* stream, bool force_tc) {
   GGNN_CHECK_ARG(X && X->d_data && d_nodes && d_offsets && nbatches >= 0, "invalid arguments");
   GGNN_CHECK_ARG(k_nn >= 1 && k_nn <= 32, "k_nn must be in [1, 32] on the GPU path");
   GGNN_CHECK_ARG(!d_adj || (d_nnd && d_dnn1 && k >= k_nn && k <= MAX_K), "layer outputs need nn_dists and d_nn1");
@@ -406,6 +545,19 @@ int ggnn_leaf_knn(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* 
   a.nnd = d_nnd;
   a.dnn1 = d_dnn1;
   a.reduced = d_reduced;
+  cudaStream_t st = as_stream(stream);
+  if (leaf_tc_eligible(X, max_batch)) {
+    const size_t smem = leaf_tc_smem(X->d);
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DevInfo di = dev_info();
+    const int per_sm = std::max(1, (int)(((size_t)di.smem_optin + 1024) / (smem + 1024)));
+    const int64_t grid = std::min<int64_t>(nbatches, (int64_t)std::max(di.sm_count, 1) * std::min(per_sm, 4));
+    leaf_knn_tc_kernel<<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+    GGNN_LAUNCH_CHECK();
+    return GGNN_OK;
+  }
+  GGNN_CHECK_ARG(!force_tc, "the tensor-core leaf kNN needs uint8 rows with d %% 32 == 0, d <= 512, batches <= %d",
+                 TC_ROWS);
   const size_t esz = X->dtype == GGNN_U8 ? 1 : 4;
   const size_t pad = X->dtype == GGNN_U8 ? 4 : 1;
   size_t want = (size_t)max_batch * (size_t)(X->d + pad) * esz;
@@ -413,7 +565,6 @@ int ggnn_leaf_knn(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* 
   size_t cap = std::min<size_t>((size_t)di.smem_optin, 160 * 1024);
   size_t smem = want <= cap ? want : 0;
   a.smem_limit = smem;
-  cudaStream_t st = as_stream(stream);
   if (X->dtype == GGNN_U8) {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     leaf_knn_kernel<uint8_t><<<(unsigned)nbatches, 256, smem, st>>>(a);
@@ -423,6 +574,26 @@ int ggnn_leaf_knn(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* 
   }
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
+}
+
+int ggnn_leaf_knn(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* d_rows, const int64_t* d_offsets,
+                  int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t* d_pos, double* d_dist, int32_t* d_adj,
+                  int32_t k, double* d_nnd, double* d_dnn1, int32_t* d_reduced, void* stream) {
+  return leaf_knn_impl(X, d_nodes, d_rows, d_offsets, nbatches, max_batch, k_nn, d_pos, d_dist, d_adj, k, d_nnd,
+                       d_dnn1, d_reduced, stream, false);
+}
+
+int ggnn_leaf_knn_tc(const ggnn_vectors* X, const int32_t* d_nodes, const int32_t* d_rows, const int64_t* d_offsets,
+                     int64_t nbatches, int64_t max_batch, int32_t k_nn, int32_t* d_pos, double* d_dist,
+                     int32_t* d_adj, int32_t k, double* d_nnd, double* d_dnn1, int32_t* d_reduced, void* stream) {
+  return leaf_knn_impl(X, d_nodes, d_rows, d_offsets, nbatches, max_batch, k_nn, d_pos, d_dist, d_adj, k, d_nnd,
+                       d_dnn1, d_reduced, stream, true);
+}
+
+int ggnn_tc_timeouts(void) {
+  int v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_tc_timeouts, sizeof(int)) != cudaSuccess) return -1;
+  return v;
 }
 
 int ggnn_merge_rows(int64_t node_count, int32_t k, int32_t k_nn, int32_t* d_adj, double* d_nnd, int32_t* d_sym_count,

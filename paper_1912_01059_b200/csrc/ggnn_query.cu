@@ -43,11 +43,21 @@ constexpr int MAX_LAYERS = 24;
 // registers at 80 per thread, so 24 searches share an SM (shared memory
 // allows about as many for the default 266-entry ring + 512-entry visited
 // ring + 1024-slot table).  Sym-check CTAs run 8 warps of small searches.
-#ifndef GGNN_SEARCH_MIN_BLOCKS
-#define GGNN_SEARCH_MIN_BLOCKS 7
+#ifndef GGNN_SEARCH_WARPS
+#define GGNN_SEARCH_WARPS 1  // one-warp CTAs: no warp waits for slower CTA-mates
 #endif
-constexpr int SEARCH_THREADS = 128;
+#ifndef GGNN_SEARCH_MIN_BLOCKS
+#define GGNN_SEARCH_MIN_BLOCKS (28 / GGNN_SEARCH_WARPS)
+#endif
+#ifndef GGNN_PERSISTENT
+#define GGNN_PERSISTENT 0  // persistent warps + work counter for the search kernels
+#endif
+constexpr int SEARCH_WARPS = GGNN_SEARCH_WARPS;
+constexpr int SEARCH_THREADS = 32 * SEARCH_WARPS;
 constexpr int SEARCH_MIN_BLOCKS = GGNN_SEARCH_MIN_BLOCKS;
+#ifndef GGNN_SYM_PERSISTENT
+#define GGNN_SYM_PERSISTENT 1
+#endif
 constexpr int SYM_THREADS = 256;
 #ifndef GGNN_SYM_MIN_BLOCKS
 #define GGNN_SYM_MIN_BLOCKS 4
@@ -97,7 +107,25 @@ struct SearchArgs {
   const int32_t* seg_of;
   int seg_div;
   int seg_size;
+  int* work;  // persistent-warp item counter (nullptr: one item per warp)
 };
+
+// Persistent warps: with a work counter (zeroed before the launch) every warp
+// takes the next item when it finishes one, so uneven search lengths never
+// leave a warp idle until its CTA-mates finish; without one each warp runs
+// its static item (one item per warp, grid covering all items).
+__device__ __forceinline__ int64_t first_item(int* work) {
+  if (!work) return (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int v = 0;
+  if (lane_id() == 0) v = atomicAdd(work, 1);
+  return (int64_t)__shfl_sync(FULL, v, 0);
+}
+__device__ __forceinline__ int64_t next_item(int* work) {
+  if (!work) return INT64_MAX;
+  int v = 0;
+  if (lane_id() == 0) v = atomicAdd(work, 1);
+  return (int64_t)__shfl_sync(FULL, v, 0);
+}
 
 template <typename TX, typename TQ>
 __device__ __forceinline__ void load_query(TQ* qs, const SearchArgs& a, int64_t qi) {
@@ -176,16 +204,12 @@ __device__ void write_hits(const WarpSearch<TX, TQ, LP>& s, const SearchArgs& a,
 
 // ------------------------------------------------------------------ query()
 template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* smem_w, int* vring_lane, int64_t qi) {
   using Key = typename VecTraits<TX, TQ>::Key;
-  const int wib = threadIdx.x >> 5;
-  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (qi >= a.m) return;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
-  VRING_DECL(s);
-  init_search(s, a, smem + (size_t)wib * a.region, qi);
+  s.vr = vring_lane;
+  init_search(s, a, smem_w, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   set_layer(s, a.layer);
   s.dmax = a.dmax;
@@ -204,18 +228,28 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kerne
   write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
 }
 
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
+  uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
+  if constexpr (GGNN_PERSISTENT != 0) {
+    for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
+      query_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+  } else {
+    const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (qi < a.m) query_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+  }
+}
+
 // ------------------------------------------------------------ greedy_search
 template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kernel(const __grid_constant__ SearchArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void greedy_kernel_one(const SearchArgs& a, uint8_t* smem_w, int* vring_lane, int64_t qi) {
   using Key = typename VecTraits<TX, TQ>::Key;
-  const int wib = threadIdx.x >> 5;
-  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (qi >= a.m) return;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
-  VRING_DECL(s);
-  init_search(s, a, smem + (size_t)wib * a.region, qi);
+  s.vr = vring_lane;
+  init_search(s, a, smem_w, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   set_layer(s, a.layer);
   s.dmax = a.dmax;
@@ -235,18 +269,28 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kern
   write_hits(s, a, qi, a.layer.to_row, 0, 0);
 }
 
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
+  uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
+  if constexpr (GGNN_PERSISTENT != 0) {
+    for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
+      greedy_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+  } else {
+    const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (qi < a.m) greedy_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+  }
+}
+
 // ------------------------------------------------------- hierarchical_query
 template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_kernel(const __grid_constant__ SearchArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t* smem_w, int* vring_lane, int64_t qi) {
   using Key = typename VecTraits<TX, TQ>::Key;
-  const int wib = threadIdx.x >> 5;
-  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (qi >= a.m) return;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
-  VRING_DECL(s);
-  init_search(s, a, smem + (size_t)wib * a.region, qi);
+  s.vr = vring_lane;
+  init_search(s, a, smem_w, qi);
   load_query<TX, TQ>(s.qs, a, qi);
   const LayerDev& Ls = a.layers[a.start];
   int lo = a.seg_lo ? __ldg(a.seg_lo + qi) : 0;
@@ -304,6 +348,20 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_ker
   }
 }
 
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
+  uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
+  if constexpr (GGNN_PERSISTENT != 0) {
+    for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
+      descent_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+  } else {
+    const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (qi < a.m) descent_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+  }
+}
+
 // ----------------------------------------------------------- sym_check_pair
 // Request records of a symmetrize pass (int32, stride REQ_HDR + n_fallback):
 //   {pair index p, x, z, d_xz low word, d_xz high word, fallback[n_fallback]}
@@ -341,15 +399,12 @@ struct SymArgs {
   bool recheck;
   int32_t* stage;
   int32_t x_end;  // recheck only requests of nodes x < x_end
+  int* work;      // persistent-warp item counter (nullptr: one item per warp)
 };
 
 template <typename TX, int LP>
-__global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(const __grid_constant__ SymArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void symcheck_kernel_one(const SymArgs& a, uint8_t* smem_w, int* vring_lane, int64_t pi) {
   using Key = typename VecTraits<TX, TX>::Key;
-  const int wib = threadIdx.x >> 5;
-  const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (pi >= a.npairs) return;
   const int lane = lane_id();
   const int rstride = REQ_HDR + a.n_fallback;
   int x, z;
@@ -389,14 +444,14 @@ __global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(c
   int v = 0;
   int cand = -1;
   WarpSearch<TX, TX, LP> s;
-  VRING_DECL(s);
+  s.vr = vring_lane;
   if (!present) {
     s.X = reinterpret_cast<const TX*>(a.X);
     s.d = a.d;
     s.lpr = a.lpr;
     s.c = a.c;
     s.target = x;
-    s.carve(smem + (size_t)wib * a.region);
+    s.carve(smem_w);
     s.ever = nullptr;
     s.ever_mask = 0;
     set_layer(s, a.layer);
@@ -445,6 +500,20 @@ __global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(c
   }
   if (keep && rank < a.n_fallback) rec[REQ_HDR + rank] = cand;
   for (int j = w + lane; j < a.n_fallback; j += 32) rec[REQ_HDR + j] = -1;
+}
+
+template <typename TX, int LP>
+__global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(const __grid_constant__ SymArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
+  uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
+  if constexpr (GGNN_SYM_PERSISTENT != 0) {
+    for (int64_t pi = first_item(a.work); pi < a.npairs; pi = next_item(a.work))
+      symcheck_kernel_one<TX, LP>(a, smem_w, vring_lane, pi);
+  } else {
+    const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (pi < a.npairs) symcheck_kernel_one<TX, LP>(a, smem_w, vring_lane, pi);
+  }
 }
 
 // ----------------------------------------------------------- exhaustive_topk
@@ -561,17 +630,61 @@ int pick_warps(size_t region, int want) {
   return ((size_t)w * region > limit) ? 0 : w;
 }
 
+// Work counters for persistent launches: a per-device pool of ints, one slot
+// per launch (round robin, zeroed on the launch's stream), so concurrent
+// launches on different streams never share a counter.
+constexpr int WORK_SLOTS = 4096;
+int* work_counter(cudaStream_t st) {
+  static std::mutex mu;
+  static int* pools[64] = {nullptr};
+  static unsigned next[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev] && cudaMalloc(&pools[dev], WORK_SLOTS * sizeof(int)) != cudaSuccess) {
+    pools[dev] = nullptr;
+    return nullptr;
+  }
+  int* slot = pools[dev] + (next[dev]++ % WORK_SLOTS);
+  if (cudaMemsetAsync(slot, 0, sizeof(int), st) != cudaSuccess) return nullptr;
+  return slot;
+}
+
+// Persistent grid: as many CTAs as fit on the device at once (never more
+// than the items need); items are handed out through a work counter.
 template <typename Kern>
-int launch_warps(Kern kern, const SearchArgs& a, int64_t items, size_t region, cudaStream_t st, int want = 4) {
+int64_t persistent_grid(Kern kern, int threads, size_t smem, int64_t items_per_cta_max) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int64_t resident = (int64_t)std::max(dev_info().sm_count, 1) * per_sm;
+  return std::min(resident, items_per_cta_max);
+}
+
+template <typename Kern, typename Args>
+int launch_items(Kern kern, Args a, int64_t items, size_t region, cudaStream_t st, int want, bool persistent = true) {
   if (items <= 0) return GGNN_OK;
   int W = pick_warps(region, want);
   GGNN_CHECK_ARG(W > 0, "search state of %zu bytes does not fit in shared memory", region);
   size_t smem = (size_t)W * region;
   GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t grid = (items + W - 1) / W;
+  a.work = persistent ? work_counter(st) : nullptr;
+  if (a.work) grid = persistent_grid(kern, W * 32, smem, grid);
   kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
+}
+
+template <typename Kern>
+int launch_warps(Kern kern, const SearchArgs& a, int64_t items, size_t region, cudaStream_t st,
+                 int want = SEARCH_WARPS) {
+  return launch_items(kern, a, items, region, st, want, GGNN_PERSISTENT != 0);
+}
+// one item per warp (kernels without a work loop)
+template <typename Kern>
+int launch_static(Kern kern, const SearchArgs& a, int64_t items, size_t region, cudaStream_t st, int want) {
+  return launch_items(kern, a, items, region, st, want, false);
 }
 
 // Launch the LP-specialised instantiation matching a.lpr (see warp_dists_t).
@@ -582,19 +695,10 @@ int launch_warps(Kern kern, const SearchArgs& a, int64_t items, size_t region, c
 
 template <typename TX>
 int launch_sym(const SymArgs& a, int64_t items, cudaStream_t st) {
-  int W = pick_warps(a.region, SYM_THREADS / 32);
-  GGNN_CHECK_ARG(W > 0, "search state does not fit in shared memory");
-  size_t smem = (size_t)W * a.region;
-  int64_t grid = (items + W - 1) / W;
-  auto go = [&](auto kern) -> int {
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
-    GGNN_LAUNCH_CHECK();
-    return GGNN_OK;
-  };
-  if (a.lpr == 8) return go(symcheck_kernel<TX, 8>);
-  if (a.lpr == 32) return go(symcheck_kernel<TX, 32>);
-  return go(symcheck_kernel<TX, 0>);
+  const bool pers = GGNN_SYM_PERSISTENT != 0;
+  if (a.lpr == 8) return launch_items(symcheck_kernel<TX, 8>, a, items, a.region, st, SYM_THREADS / 32, pers);
+  if (a.lpr == 32) return launch_items(symcheck_kernel<TX, 32>, a, items, a.region, st, SYM_THREADS / 32, pers);
+  return launch_items(symcheck_kernel<TX, 0>, a, items, a.region, st, SYM_THREADS / 32, pers);
 }
 
 int qelem_of(int dtype) { return dtype == GGNN_U8 ? 1 : 4; }
@@ -903,9 +1007,15 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   a.region = 128 + align16(32 * (size_t)keysize) + align16((size_t)X->d * qelem_of(qd));
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return GGNN_LAUNCH_LP(topk_kernel, float, float, a, a.m, a.region, st, 8);
-    case 1: return GGNN_LAUNCH_LP(topk_kernel, uint8_t, uint8_t, a, a.m, a.region, st, 8);
-    default: return launch_warps(topk_kernel<uint8_t, float, 0>, a, a.m, a.region, st, 8);
+    case 0:
+      if (a.lpr == 32) return launch_static(topk_kernel<float, float, 32>, a, a.m, a.region, st, 8);
+      if (a.lpr == 8) return launch_static(topk_kernel<float, float, 8>, a, a.m, a.region, st, 8);
+      return launch_static(topk_kernel<float, float, 0>, a, a.m, a.region, st, 8);
+    case 1:
+      if (a.lpr == 32) return launch_static(topk_kernel<uint8_t, uint8_t, 32>, a, a.m, a.region, st, 8);
+      if (a.lpr == 8) return launch_static(topk_kernel<uint8_t, uint8_t, 8>, a, a.m, a.region, st, 8);
+      return launch_static(topk_kernel<uint8_t, uint8_t, 0>, a, a.m, a.region, st, 8);
+    default: return launch_static(topk_kernel<uint8_t, float, 0>, a, a.m, a.region, st, 8);
   }
 }
 

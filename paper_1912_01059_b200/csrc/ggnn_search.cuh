@@ -79,6 +79,13 @@ inline int table_log2(int cap, int vsz) {
   return lg;
 }
 
+// 128-byte lines of each neighbour row prefetched into L1 at the start of an
+// expansion (0 disables; rows longer than this are only partly prefetched)
+#ifndef GGNN_PREFETCH_LINES
+#define GGNN_PREFETCH_LINES 1
+#endif
+constexpr int PREFETCH_LINES = GGNN_PREFETCH_LINES;
+
 template <typename TX, typename TQ, int LP = 0>
 struct WarpSearch {
   using Key = typename VecTraits<TX, TQ>::Key;
@@ -112,6 +119,9 @@ struct WarpSearch {
   uint32_t ever_mask;
   // warp-uniform state
   int L, vlen, vpos, used, rebuild_at;
+  // adjacency row of the predicted next expansion, loaded while the current
+  // step merges (pf_nb: this lane's slot of row pf_node)
+  int pf_node, pf_nb;
   int visited, steps, distinct, forgotten, term;
   bool found_target;
 
@@ -145,6 +155,8 @@ struct WarpSearch {
     ht.clear();
     L = vlen = vpos = used = 0;
     rebuild_at = (int)((ht.mask + 1) * 3 / 4);
+    pf_node = -1;
+    pf_nb = -1;
     visited = steps = distinct = forgotten = 0;
     term = TERM_EMPTY;
     found_target = false;
@@ -188,15 +200,18 @@ struct WarpSearch {
   }
 
   // ring position of the first unvisited entry, -1 if none
-  __device__ int head() const {
+  __device__ int head() const { return head_from(0); }
+
+  // first unvisited ring position >= start (start a multiple of 4 or not), -1 if none
+  __device__ int head_from(int start) const {
     const int lane = lane_id();
-    for (int base = 0; base < L; base += 128) {
+    for (int base = start & ~3; base < L; base += 128) {
       int p0 = base + 4 * lane;
       uint32_t w = *reinterpret_cast<const uint32_t*>(rvis + p0);
       int fb = 4;
 #pragma unroll
       for (int b = 3; b >= 0; --b)
-        if (p0 + b < L && ((w >> (8 * b)) & 0xffu) == 0u) fb = b;
+        if (p0 + b < L && p0 + b >= start && ((w >> (8 * b)) & 0xffu) == 0u) fb = b;
       unsigned bal = __ballot_sync(FULL, fb < 4);
       if (bal) {
         int src = __ffs(bal) - 1;
@@ -354,7 +369,24 @@ struct WarpSearch {
     ht.inc((uint32_t)node);
 
     int nb = -1;
-    if (lane < k) nb = __ldg(adj + (int64_t)node * k + lane);
+    if (node == pf_node) {
+      nb = pf_nb;
+    } else if (lane < k) {
+      nb = __ldg(adj + (int64_t)node * k + lane);
+    }
+    pf_node = -1;
+    // start pulling every neighbour's row towards L1 now; the membership
+    // filter below usually keeps about half of them
+    int nrow = -1;
+    if (nb >= 0) {
+      nrow = to_row ? __ldg(to_row + nb) : nb;
+      if (PREFETCH_LINES > 0) {
+        const char* rp = reinterpret_cast<const char*>(X + (int64_t)nrow * d);
+#pragma unroll
+        for (int l = 0; l < PREFETCH_LINES; ++l)
+          if (l * 128 < d * (int64_t)sizeof(TX)) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + l * 128));
+      }
+    }
     bool cand = nb >= 0;
     if (cand) cand = ht.count((uint32_t)nb) == 0u;
     unsigned same = __match_any_sync(FULL, cand ? (unsigned)nb : (0x80000000u | (unsigned)lane));
@@ -365,7 +397,7 @@ struct WarpSearch {
     if (nc) {
       const int ci = __popc(cm & lanemask_lt());
       if (cand) {
-        crow[ci] = to_row ? __ldg(to_row + nb) : nb;
+        crow[ci] = nrow;
         cid[ci] = nb;
       }
       __syncwarp();
@@ -385,7 +417,13 @@ struct WarpSearch {
       const int m = __popc(__ballot_sync(FULL, adm));
       forgotten += nc - m;
       if (target >= 0) found = __any_sync(FULL, adm && id == target);
+      // predict the next expansion -- the smaller of the next unvisited ring
+      // entry and the best admitted candidate -- and load its adjacency row
+      // while the merge runs (checked against the real head next step)
+      if (!found) prefetch_next(pos, m > 0, KO::shfl(key, 0), __shfl_sync(FULL, id, 0));
       if (m) merge(key, id, m);
+    } else {
+      prefetch_next(pos, false, KO::max_key(), INT_MAX);
     }
     steps++;
     if (found) {
@@ -394,6 +432,22 @@ struct WarpSearch {
       return false;
     }
     return true;
+  }
+
+  __device__ __forceinline__ void prefetch_next(int pos, bool have_cand, Key kc, int ic) {
+    const int q = head_from(pos + 1);
+    Key ko = KO::max_key();
+    int io = INT_MAX;
+    if (q >= 0) {
+      ko = rk[q];
+      io = rid[q];
+    }
+    int pred = io;
+    if (have_cand && key_less(kc, ic, ko, io)) pred = ic;
+    if (pred != INT_MAX) {
+      pf_node = pred;
+      pf_nb = lane_id() < k ? __ldg(adj + (int64_t)pred * k + lane_id()) : -1;
+    }
   }
 
   __device__ void run() {

@@ -254,3 +254,39 @@ def test_gpu_built_sift10k_recall_parity(golden_sift):
     adj = h.layers[0].adjacency
     c10 = np.mean([len(set(adj[x, :10]) & set([v for v in knn[i] if v != x][:10])) / 10 for i, x in enumerate(sample)])
     assert c10 >= 0.95, c10
+
+
+@pytest.mark.parametrize("d", [32, 128, 256])
+def test_leaf_knn_tensor_cores_vs_checker(d):
+    """tcgen05 kind::i8 leaf kNN (ggnn_leaf_knn_tc): positions and distances
+    equal the reference's batch_bruteforce (CPU checker) on integer data with
+    heavy distance ties, for batch sizes 2..128."""
+    from paper_1912_01059_b200 import _native as N
+    from paper_1912_01059_b200.device import DeviceVectors
+
+    rng = np.random.default_rng(d)
+    sizes = np.concatenate([[2, 3, 16, 17, 128, 127, 64], rng.integers(2, 129, size=33)])
+    n = int(sizes.sum()) + 50
+    X = rng.integers(0, 4 if d == 32 else 256, size=(n, d)).astype(np.float32)
+    X.setflags(write=False)
+    members = rng.permutation(n)[: sizes.sum()].astype(np.int32)
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    k_nn = 12
+    dv = DeviceVectors.of_array(X)
+    assert dv.exact_integers
+    t = N.torch()
+    pos = N.empty((len(members), k_nn), t.int32)
+    dist = N.empty((len(members), k_nn), t.float64)
+    red = t.zeros(1, dtype=t.int32, device=N.device())
+    mem_d, off_d = N.to_dev(members), N.to_dev(offsets)  # keep the device copies alive across the launch
+    N.call("ggnn_leaf_knn_tc", N.ctypes.byref(dv.struct), N.ptr(mem_d), None, N.ptr(off_d),
+           len(sizes), int(sizes.max()), k_nn, N.ptr(pos), N.ptr(dist), None, 0, None, None, N.ptr(red),
+           N.stream_ptr())
+    pos, dist = pos.cpu().numpy(), dist.cpu().numpy()
+    assert N.load().ggnn_tc_timeouts() == 0
+    assert int(red.item()) == int((sizes < k_nn + 1).sum())
+    for b in range(len(sizes)):
+        lo, hi = offsets[b], offsets[b + 1]
+        p_ref, d_ref = O.batch_bruteforce(X, members[lo:hi], k_nn)
+        np.testing.assert_array_equal(pos[lo:hi], p_ref)
+        np.testing.assert_array_equal(dist[lo:hi], d_ref)
