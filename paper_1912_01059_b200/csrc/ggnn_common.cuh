@@ -384,6 +384,18 @@ struct RefTable {
     if (s >= 0 && lane_id() == 0) t[s] = TOMB;
     __syncwarp();
   }
+  // per-lane tombstoning of a live key with count 1 (distinct keys per lane)
+  __device__ __forceinline__ void tomb_lane(uint32_t key) {
+    uint32_t s = home(key);
+    for (;;) {
+      const uint32_t v = t[s];
+      if (v != TOMB && v != EMPTY && (v & KMASK) == key) {
+        t[s] = TOMB;
+        return;
+      }
+      s = (s + 1) & mask;
+    }
+  }
   __device__ __forceinline__ void clear() {
     for (uint32_t i = lane_id(); i <= mask; i += 32) t[i] = EMPTY;
     __syncwarp();

@@ -250,6 +250,28 @@ struct WarpSearch {
     __syncwarp();
   }
 
+  // Drop the E (<= 32) largest ring entries, largest first (_core.pyx:161-166).
+  // Unvisited ones have refcount exactly 1 and vanish (forgotten); their table
+  // slots are tombstoned lane-parallel.  Visited ones go to the visited ring
+  // in eviction order (their +1 there and -1 here cancel).
+  __device__ __forceinline__ void evict(int E) {
+    const int lane = lane_id();
+    const bool in = lane < E;
+    const int r = L - 1 - lane;
+    const int t = in ? rid[r] : -1;
+    const bool vis = in && rvis[r] != 0;
+    const bool gone = in && !vis;
+    if (gone) ht.tomb_lane((uint32_t)t);
+    forgotten += __popc(__ballot_sync(FULL, gone));
+    __syncwarp();
+    unsigned vm = __ballot_sync(FULL, vis);
+    while (vm) {
+      const int e = __ffs(vm) - 1;
+      vm &= vm - 1;
+      vring_push(__shfl_sync(FULL, t, e));
+    }
+  }
+
   // Lanes [0, m) hold ascending, distinct, currently-unknown (key, id) pairs.
   // Equivalent to calling the reference's _ring_insert on each in order.
   __device__ void merge(Key key, int id, int m) {
@@ -274,47 +296,38 @@ struct WarpSearch {
     if (madm == 0) return;
     const int newL = min(c.cap, L + madm);
     const int E = L + madm - newL;
-    // evictions, largest first (_core.pyx:161-166)
-    for (int e = 0; e < E; ++e) {
-      const int r = L - 1 - e;
-      const int t = rid[r];
-      const bool vis = rvis[r] != 0;
-      if (vis) {
-        // push t onto the visited ring; its +1 and the ring's -1 cancel
-        vring_push(t);
-      } else {
-        ht.tomb((uint32_t)t);  // unvisited ring entries have count exactly 1
-        forgotten++;
-      }
-    }
-    // shift kept entries [rank_0, L-E) right by s_r = #{i : rank_i <= r}
-    const int Lkeep = L - E;
-    const int r0 = __shfl_sync(FULL, rank, 0);
-    for (int hi = Lkeep; hi > r0; hi -= 32) {
-      const int r = hi - 32 + lane;
-      const bool act = r >= r0;
-      Key kk = Key(0);
-      int ii = 0;
+    if (E > 0) evict(E);
+    // Scatter the merged sequence in place, top chunk first: output position
+    // o holds the candidate whose slot is o, else ring entry o - #{candidates
+    // placed below o}.  Every source index is <= its destination and chunks
+    // go downwards, so nothing is overwritten before it is read.
+    const int p0 = __shfl_sync(FULL, p, 0);
+    for (int hi = newL; hi > p0; hi -= 32) {
+      const int cb = hi - 32;
+      const int o = cb + lane;
+      const bool act = o >= p0;
+      const unsigned bit = (ok && p >= cb && p < hi) ? (1u << (p - cb)) : 0u;
+      const unsigned cmask = __reduce_or_sync(FULL, bit);
+      const int below = __popc(__ballot_sync(FULL, ok && p < cb)) + __popc(cmask & lanemask_lt());
+      const bool is_c = (cmask >> lane) & 1u;
+      const Key ck = KO::shfl(key, below & 31);
+      const int ci = __shfl_sync(FULL, id, below & 31);
+      Key kk = ck;
+      int ii = ci;
       uint8_t vv = 0;
-      if (act) {
+      if (act && !is_c) {
+        const int r = o - below;
         kk = rk[r];
         ii = rid[r];
         vv = rvis[r];
       }
-      int s = 0;
-      for (int i = 0; i < madm; ++i) s += (__shfl_sync(FULL, rank, i) <= r) ? 1 : 0;
       __syncwarp();
       if (act) {
-        rk[r + s] = kk;
-        rid[r + s] = ii;
-        rvis[r + s] = vv;
+        rk[o] = kk;
+        rid[o] = ii;
+        rvis[o] = vv;
       }
       __syncwarp();
-    }
-    if (ok) {
-      rk[p] = key;
-      rid[p] = id;
-      rvis[p] = 0;
     }
     int took = ok ? ht.insert_new((uint32_t)id) : 0;
     used += warp_sum(took);
