@@ -75,6 +75,43 @@ __device__ __forceinline__ void warp_sort(K& key, int& id) {
   }
 }
 
+// Exact integer keys pack with their id into one u64 whose unsigned order is
+// the (key, id) order (ids are >= 0, padding uses INT_MAX): one compare and
+// one 64-bit exchange per network stage.
+__device__ __forceinline__ uint64_t pack_ki(uint32_t key, int id) {
+  return ((uint64_t)key << 32) | (uint64_t)(uint32_t)id;
+}
+
+// Bitonic sort of the first `width` (16 or 32) lanes, ascending; for width 16
+// lanes 16..31 must hold values >= every lane below (the padding).
+__device__ __forceinline__ void warp_sort_u64(uint64_t& v, int width) {
+  const int lane = lane_id();
+  for (int size = 2; size <= width; size <<= 1) {
+#pragma unroll
+    for (int stride = 16; stride > 0; stride >>= 1) {
+      if (stride >= size) continue;
+      const uint64_t o = __shfl_xor_sync(FULL, v, stride);
+      const bool up = ((lane & size) == 0);
+      const bool lower = ((lane & stride) == 0);
+      // lower lane of an ascending pair keeps the min, of a descending pair the max
+      v = (lower == up) ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  }
+}
+
+// Sort of the first n (<= 32) (key, id) lanes, padding (max, INT_MAX) above n.
+template <typename K>
+__device__ __forceinline__ void warp_sort_n(K& key, int& id, int n) {
+  if constexpr (sizeof(K) == 4) {
+    uint64_t v = pack_ki(key, id);
+    warp_sort_u64(v, n <= 16 ? 16 : 32);
+    key = (K)(v >> 32);
+    id = (int)(uint32_t)v;
+  } else {
+    warp_sort(key, id);
+  }
+}
+
 // ---------------------------------------------------------------- vectors
 // Query storage: float queries are kept as float in shared memory, uint8
 // queries as uint8.  Distances:

@@ -466,7 +466,7 @@ __device__ __forceinline__ void symcheck_kernel_one(const SymArgs& a, uint8_t* s
     v = s.term ? 1 : 2;
     // fallbacks: closest explored ids excluding x and z (_core.pyx:420-426)
     const int nh = min(s.L, a.c.k_out);
-    if (v == 2 && lane < nh) cand = s.rid[lane];
+    if (v == 2 && lane < nh) cand = s.ring_id(lane);
   }
   if (lane == 0 && a.verdict) a.verdict[pi] = v;
   const bool keep = cand >= 0 && cand != x && cand != z;

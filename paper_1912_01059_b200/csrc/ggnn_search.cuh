@@ -104,7 +104,10 @@ struct WarpSearch {
   // config
   SearchCfg c;
   int target;  // -1: normal mode
-  // shared memory
+  // shared memory: the ring as packed (key << 32 | id) words for exact
+  // integer keys (PACK), as separate key / id arrays otherwise
+  static constexpr bool PACK = sizeof(Key) == 4;
+  uint64_t* re;
   Key* rk;
   int* rid;
   uint8_t* rvis;
@@ -125,12 +128,26 @@ struct WarpSearch {
   int visited, steps, distinct, forgotten, term;
   bool found_target;
 
+  __device__ __forceinline__ Key ring_key(int i) const {
+    if constexpr (PACK) return (Key)(re[i] >> 32);
+    else return rk[i];
+  }
+  __device__ __forceinline__ int ring_id(int i) const {
+    if constexpr (PACK) return (int)(uint32_t)re[i];
+    else return rid[i];
+  }
+
   __device__ void carve(uint8_t* base) {
     uint8_t* p = base;
-    rk = reinterpret_cast<Key*>(p);
-    p += align16((size_t)c.cap * sizeof(Key));
-    rid = reinterpret_cast<int*>(p);
-    p += align16((size_t)c.cap * 4);
+    if constexpr (PACK) {
+      re = reinterpret_cast<uint64_t*>(p);
+      p += align16((size_t)c.cap * sizeof(Key)) + align16((size_t)c.cap * 4);
+    } else {
+      rk = reinterpret_cast<Key*>(p);
+      p += align16((size_t)c.cap * sizeof(Key));
+      rid = reinterpret_cast<int*>(p);
+      p += align16((size_t)c.cap * 4);
+    }
     rvis = p;
     p += align16((size_t)((c.cap + 127) / 128) * 128);
     vring = nullptr;
@@ -189,7 +206,7 @@ struct WarpSearch {
     const int lane = lane_id();
     ht.clear();
     int u = 0;
-    for (int i = lane; i < L; i += 32) u += ht.add_one((uint32_t)rid[i]);
+    for (int i = lane; i < L; i += 32) u += ht.add_one((uint32_t)ring_id(i));
     for (int i = lane; i < vlen; i += 32) u += ht.add_one((uint32_t)(vring ? vring[i] : vr[i >> 5]));
     used = warp_sum(u);
     // next purge once tombstones fill an eighth of the table, never so late
@@ -258,7 +275,7 @@ struct WarpSearch {
     const int lane = lane_id();
     const bool in = lane < E;
     const int r = L - 1 - lane;
-    const int t = in ? rid[r] : -1;
+    const int t = in ? ring_id(r) : -1;
     const bool vis = in && rvis[r] != 0;
     const bool gone = in && !vis;
     if (gone) ht.tomb_lane((uint32_t)t);
@@ -279,13 +296,24 @@ struct WarpSearch {
     int rank = 0;
     if (lane < m) {
       int lo = 0, hi = L;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        Key km = rk[mid];
-        if (km < key || (km == key && rid[mid] <= id))
-          lo = mid + 1;
-        else
-          hi = mid;
+      if constexpr (PACK) {
+        const uint64_t pk = pack_ki((uint32_t)key, id);
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (re[mid] <= pk)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+      } else {
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const Key km = rk[mid];
+          if (km < key || (km == key && rid[mid] <= id))
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
       }
       rank = lo;
     }
@@ -310,22 +338,37 @@ struct WarpSearch {
       const unsigned cmask = __reduce_or_sync(FULL, bit);
       const int below = __popc(__ballot_sync(FULL, ok && p < cb)) + __popc(cmask & lanemask_lt());
       const bool is_c = (cmask >> lane) & 1u;
-      const Key ck = KO::shfl(key, below & 31);
-      const int ci = __shfl_sync(FULL, id, below & 31);
-      Key kk = ck;
-      int ii = ci;
-      uint8_t vv = 0;
-      if (act && !is_c) {
-        const int r = o - below;
-        kk = rk[r];
-        ii = rid[r];
-        vv = rvis[r];
-      }
-      __syncwarp();
-      if (act) {
-        rk[o] = kk;
-        rid[o] = ii;
-        rvis[o] = vv;
+      if constexpr (PACK) {
+        uint64_t ee = __shfl_sync(FULL, pack_ki((uint32_t)key, id), below & 31);
+        uint8_t vv = 0;
+        if (act && !is_c) {
+          const int r = o - below;
+          ee = re[r];
+          vv = rvis[r];
+        }
+        __syncwarp();
+        if (act) {
+          re[o] = ee;
+          rvis[o] = vv;
+        }
+      } else {
+        const Key ck = KO::shfl(key, below & 31);
+        const int ci = __shfl_sync(FULL, id, below & 31);
+        Key kk = ck;
+        int ii = ci;
+        uint8_t vv = 0;
+        if (act && !is_c) {
+          const int r = o - below;
+          kk = rk[r];
+          ii = rid[r];
+          vv = rvis[r];
+        }
+        __syncwarp();
+        if (act) {
+          rk[o] = kk;
+          rid[o] = ii;
+          rvis[o] = vv;
+        }
       }
       __syncwarp();
     }
@@ -351,7 +394,7 @@ struct WarpSearch {
     const int cnt = __popc(__ballot_sync(FULL, v));
     if (ever) distinct += warp_sum(ever_insert(v ? id : -1));
     else distinct += cnt;
-    warp_sort(key, id);
+    warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n)
     if (cnt) merge(key, id, cnt);
   }
 
@@ -366,8 +409,9 @@ struct WarpSearch {
     double thr = __longlong_as_double(0x7ff0000000000000ll);
     // FP64, rounded exactly like the reference (no FMA contraction):
     // thr = ring[k_out-1] + tau * min(d_nn1_max, ring[0])   (_core.pyx:241-244)
-    if (L >= c.k_out) thr = __dadd_rn(KO::to_d(rk[c.k_out - 1]), __dmul_rn(c.tau, fmin(dmax, KO::to_d(rk[0]))));
-    if (KO::to_d(rk[pos]) > thr) {
+    if (L >= c.k_out)
+      thr = __dadd_rn(KO::to_d(ring_key(c.k_out - 1)), __dmul_rn(c.tau, fmin(dmax, KO::to_d(ring_key(0)))));
+    if (KO::to_d(ring_key(pos)) > thr) {
       term = TERM_STOP;
       return false;
     }
@@ -375,7 +419,7 @@ struct WarpSearch {
       term = TERM_CAP;
       return false;
     }
-    const int node = rid[pos];
+    const int node = ring_id(pos);
     __syncwarp();
     if (lane == 0) rvis[pos] = 1;
     vring_push(node);
@@ -425,7 +469,7 @@ struct WarpSearch {
       __syncwarp();
       visited += nc;
       if (ever) distinct += warp_sum(ever_insert(lane < nc ? id : -1));
-      warp_sort(key, id);
+      warp_sort_n(key, id, nc);
       const bool adm = lane < nc && KO::to_d(key) <= thr;
       const int m = __popc(__ballot_sync(FULL, adm));
       forgotten += nc - m;
@@ -452,8 +496,8 @@ struct WarpSearch {
     Key ko = KO::max_key();
     int io = INT_MAX;
     if (q >= 0) {
-      ko = rk[q];
-      io = rid[q];
+      ko = ring_key(q);
+      io = ring_id(q);
     }
     int pred = io;
     if (have_cand && key_less(kc, ic, ko, io)) pred = ic;
@@ -476,8 +520,8 @@ struct WarpSearch {
     key = KO::max_key();
     id = -1;
     if (lane < nh) {
-      key = rk[lane];
-      id = rid[lane];
+      key = ring_key(lane);
+      id = ring_id(lane);
     }
     return nh;
   }
