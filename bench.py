@@ -364,9 +364,10 @@ def main():
     torch.cuda.synchronize()
     e2e_t = dist.max(time.perf_counter() - t0)
     e2e = {"value": args.gpus * m * args.steps / e2e_t, "unit": UNIT,
-           "h2d_bytes_per_step": int(m * d * (1 if dv.exact_integers else 4)),
-           "d2h_bytes_per_step": int(out.ids.nbytes + out.dists.nbytes + out.counters.nbytes),
-           "api": "paper_1912_01059_b200.query_arrays(h, numpy queries) -> host arrays"}
+           "h2d_bytes_per_step": int(Q_host.nbytes),
+           "d2h_bytes_per_step": int(out.ids.nbytes + out.dists.nbytes + out.counters.nbytes + 4),
+           "api": "paper_1912_01059_b200.query_arrays(h, numpy float32 queries) -> host arrays (pinned staging, "
+                  "float32 upload narrowed to uint8 on the device)"}
 
     # ---- CPU baseline (rank 0, N == 1) ---------------------------------
     cpu = None

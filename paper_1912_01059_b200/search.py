@@ -90,6 +90,69 @@ def _check_query(h, q: np.ndarray) -> np.ndarray:
     return q
 
 
+class _Staging:
+    """Reusable pinned host / device buffers of the host-to-host query path
+    (one per device): the query batch goes host -> pinned -> device once as
+    float32, is narrowed to uint8 on the device when every value is an
+    integer in [0, 255] (ggnn_f32_to_u8), and the results come back through
+    pinned buffers -- no per-call allocations, one synchronisation."""
+
+    def __init__(self):
+        self.m = self.d = self.k = 0
+
+    def ensure(self, m: int, d: int, k: int):
+        if m <= self.m and d == self.d and k == self.k:
+            return self
+        t = N.torch()
+        m = max(m, self.m if (d == self.d and k == self.k) else 0)
+        self.m, self.d, self.k = m, d, k
+        self.q_pin = t.empty((m, d), dtype=t.float32, pin_memory=True)
+        self.ids_pin = t.empty((m, k), dtype=t.int32, pin_memory=True)
+        self.dists_pin = t.empty((m, k), dtype=t.float64, pin_memory=True)
+        self.cnt_pin = t.empty((m, 5), dtype=t.int32, pin_memory=True)
+        self.flag_pin = t.empty((1,), dtype=t.int32, pin_memory=True)
+        self.q_f32 = N.empty((m, d), t.float32)
+        self.q_u8 = N.empty((m, d), t.uint8)
+        self.ids = N.empty((m, k), t.int32)
+        self.dists = N.empty((m, k), t.float64)
+        self.cnt = N.empty((m, 5), t.int32)
+        self.flag = N.empty((1,), t.int32)
+        return self
+
+
+_STAGING: dict = {}
+
+
+def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
+    t = N.torch()
+    dv = dh.vectors
+    m, d = Q.shape
+    k = cfg.k_out
+    dev = t.cuda.current_device()
+    st = _STAGING.setdefault(dev, _Staging()).ensure(m, d, k)
+    stream = t.cuda.current_stream()
+    np.copyto(st.q_pin[:m].numpy(), Q)
+    st.q_f32[:m].copy_(st.q_pin[:m], non_blocking=True)
+    qs = N.queries_struct(data=st.q_f32, dtype_code=N.GGNN_F32, m=m)
+    if dv.exact_integers:
+        st.flag.fill_(1)
+        N.call("ggnn_f32_to_u8", N.ptr(st.q_f32), m * d, N.ptr(st.q_u8), N.ptr(st.flag), N.stream_ptr())
+        st.flag_pin.copy_(st.flag, non_blocking=True)
+        stream.synchronize()
+        if int(st.flag_pin[0]) == 1:
+            qs = N.queries_struct(data=st.q_u8, dtype_code=N.GGNN_U8, m=m)
+    params = _params(cfg, _flags(dv, False))
+    N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct), N.ptr(dh.top_rows),
+           dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, N.ptr(st.ids), N.ptr(st.dists),
+           N.ptr(st.cnt), None, 0, N.stream_ptr())
+    st.ids_pin[:m].copy_(st.ids[:m], non_blocking=True)
+    st.dists_pin[:m].copy_(st.dists[:m], non_blocking=True)
+    st.cnt_pin[:m].copy_(st.cnt[:m], non_blocking=True)
+    stream.synchronize()
+    return BatchResult(st.ids_pin[:m].numpy().copy(), st.dists_pin[:m].numpy().copy(),
+                       st.cnt_pin[:m].numpy().copy())
+
+
 def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinct: bool = False,
                  out: str = "numpy"):
     """Batched query(): top-layer scan + best-first search on layer 0 for every
@@ -103,6 +166,8 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
         Q = Q[None, :]
     if Q.shape[1] != dv.d:
         raise ValueError(f"query dimension {Q.shape[1]} does not match index dimension {dv.d}")
+    if not distinct and out == "numpy" and Q.shape[0] > 0:
+        return _query_host_fast(dh, Q, cfg)
     m = Q.shape[0]
     t = N.torch()
     ids = N.empty((m, cfg.k_out), t.int32)

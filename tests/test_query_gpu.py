@@ -178,3 +178,29 @@ def test_hierarchical_query_matches_checker(golden_int):
         np.testing.assert_array_equal(r.dists, dists)
         assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten) == (
             v, t, term, dist_cnt, fg)
+
+
+def test_query_arrays_integral_and_fractional_queries(golden_sift):
+    """The host-to-host path narrows integral queries to uint8 on the device;
+    fractional queries against the uint8 table stay float (FP64 distances,
+    returned hits re-scored sequentially like _sqdist)."""
+    g, h, queries = golden_sift
+    cfg = ga.QueryConfig(k_out=10, tau=0.6)
+    a = ga.query_arrays(h, queries, cfg)
+    np.testing.assert_array_equal(a.ids, g["q6_ids"])
+    np.testing.assert_array_equal(a.dists, g["q6_dists"])
+    np.testing.assert_array_equal(a.counters[:, :3], g["q6_cnt"][:, :3])
+    Qf = (queries + 0.25).astype(np.float32)
+    b = ga.query_arrays(h, Qf, cfg)
+    layers = [(L.adjacency, L.k_nn, L.sym_count) for L in h.layers]
+    X = h.dataset.vectors
+    same = 0
+    for i in range(len(Qf)):
+        ids, dd, v, t, term, _, _ = O.query(layers, h.to_bottom, X, Qf[i], 10, 0.6, h.stats.d_nn1_max)
+        for node, dist in zip(b.ids[i], b.dists[i]):
+            if node >= 0:
+                assert O.squared_l2(Qf[i], X[node]) == dist
+        if np.array_equal(b.ids[i, :len(ids)], ids):
+            same += 1
+            np.testing.assert_array_equal(b.dists[i, :len(dd)], dd)
+    assert same >= 0.98 * len(Qf)
