@@ -291,7 +291,10 @@ def main():
     h, bstats = ga.build(ds, cfg)
     build_s = dist.max(bstats.build_seconds)
 
-    gt_ids, _ = ga.search.exact_knn(ds, Q, 10)
+    torch.cuda.synchronize()
+    t_gt = time.perf_counter()
+    gt_ids, _ = ga.search.exact_knn(ds, Q, 10)  # tcgen05 brute force (exact u8 distances)
+    gt_s = time.perf_counter() - t_gt
     chosen, sweep = choose_tau(ga, h, Q, gt_ids, args.tau)
     tau = chosen["tau"]
     qcfg = ga.QueryConfig(k_out=10, tau=tau)
@@ -394,7 +397,8 @@ def main():
         "config": {"workload": f"SIFT1M-shaped latent16 {args.n}x{args.d}, {m} queries/rank, k=10, k_build=24",
                    "tau": tau, "recall": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
                    "mean_visited": chosen["V"], "mean_steps": chosen["T"], "tau_sweep": sweep,
-                   "build_seconds": build_s, "build_phase_seconds_top": dict(sorted(
+                   "build_seconds": build_s, "ground_truth_seconds": gt_s,
+                   "build_phase_seconds_top": dict(sorted(
                        bstats.phase_seconds.items(), key=lambda kv: -kv[1])[:6]),
                    "parallelism": f"replicas x{args.gpus} (independent query batches)",
                    "l2": "inputs larger than L2 (u8 vectors 128 MB + adjacency 96 MB)"},

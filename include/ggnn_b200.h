@@ -147,6 +147,18 @@ int ggnn_sym_check_batch(const ggnn_vectors *X, const ggnn_layer *layer, const i
 int ggnn_exhaustive_topk(const ggnn_vectors *X, const int32_t *d_rows, int64_t nrows, const ggnn_queries *Q,
                          int32_t k, int32_t *d_ids, double *d_dists, void *stream);
 
+/* Same contract as ggnn_exhaustive_topk over the whole table, forced onto the
+ * tcgen05 path (kind::i8 MMA of 128-query tiles against streamed 256-row
+ * tiles, exact integer distances, top-k epilogue from TMEM); GGNN_E_INVALID
+ * unless X and Q are uint8, d % 32 == 0, d <= 224, 1 <= k <= 32.
+ * ggnn_exhaustive_topk takes this path by itself for such whole-table scans
+ * of at least 4096 rows. */
+int ggnn_exhaustive_topk_tc(const ggnn_vectors *X, const ggnn_queries *Q, int32_t k, int32_t *d_ids,
+                            double *d_dists, void *stream);
+
+/* Tensor-core brute-force tiles whose MMA wait timed out since load (0 when healthy). */
+int ggnn_bf_timeouts(void);
+
 /* Replaces: squared_l2_many (_core.pyx:47-55): exact sequential FP64
  * distances of query i to rows d_rows[i*per_query + j]. */
 int ggnn_squared_l2_many(const ggnn_vectors *X, const ggnn_queries *Q, const int32_t *d_rows, int32_t per_query,

@@ -63,6 +63,8 @@ _SIGS = {
     "ggnn_descent_batch": [P, P, I32, I32, I32, P, P, P, P, P, P, P, P, ctypes.c_size_t, P],
     "ggnn_sym_check_batch": [P, P, P, P, P, I64, F64, F64, I32, I32, I32, I32, I32, P, P, P],
     "ggnn_exhaustive_topk": [P, P, I64, P, I32, P, P, P],
+    "ggnn_exhaustive_topk_tc": [P, P, I32, P, P, P],
+    "ggnn_bf_timeouts": [],
     "ggnn_squared_l2_many": [P, P, P, I32, P, P],
     "ggnn_f32_to_u8": [P, I64, P, P, P],
     "ggnn_leaf_knn": [P, P, P, P, I64, I64, I32, P, P, P, I32, P, P, P, P],

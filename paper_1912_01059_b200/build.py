@@ -29,7 +29,7 @@ SYM_CHECK_VISITED = 128
 SYM_FALLBACK = 8
 # node windows per symmetrize pass: requests of x-window w are re-checked after the
 # claims of windows < w, approximating the reference's sequential x order
-SYM_WINDOWS = 16
+SYM_WINDOWS = int(__import__("os").environ.get("GGNN_SYM_WINDOWS", "16"))
 CONSENSUS_SAMPLE = 256
 CONSENSUS_K = 10
 

@@ -16,6 +16,11 @@
 
 namespace ggnn {
 
+// tensor-core brute force (ggnn_bf_tc.cu)
+bool bf_tc_eligible(const ggnn_vectors* X, const int32_t* d_rows, const ggnn_queries* Q, int k);
+int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_ids, double* d_dists,
+               cudaStream_t st);
+
 static thread_local std::string g_err;
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -998,6 +1003,9 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   int rc = fill_common(a, X, Q, &p);
   if (rc) return rc;
   GGNN_CHECK_ARG(nrows >= 1 && nrows <= INT32_MAX, "invalid row count");
+  // whole-table scans of uint8 data at least one X tile per split long: tensor cores
+  if (bf_tc_eligible(X, d_rows, Q, k) && nrows == X->n && X->n >= 4096)
+    return bf_topk_tc(X, Q, k, d_ids, d_dists, as_stream(stream));
   a.top_rows = d_rows;
   a.ntop = nrows;
   a.ids = d_ids;
@@ -1017,6 +1025,17 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
       return launch_static(topk_kernel<uint8_t, uint8_t, 0>, a, a.m, a.region, st, 8);
     default: return launch_static(topk_kernel<uint8_t, float, 0>, a, a.m, a.region, st, 8);
   }
+}
+
+int ggnn_exhaustive_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int32_t k, int32_t* d_ids,
+                            double* d_dists, void* stream) {
+  ggnn_search_params p{k, 1, 1, 0, 0.0, 0};
+  SearchArgs a;
+  int rc = fill_common(a, X, Q, &p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(bf_tc_eligible(X, nullptr, Q, k),
+                 "the tensor-core scan needs uint8 table and queries, d %% 32 == 0, d <= 224, k in [1, 32]");
+  return bf_topk_tc(X, Q, k, d_ids, d_dists, as_stream(stream));
 }
 
 int ggnn_squared_l2_many(const ggnn_vectors* X, const ggnn_queries* Q, const int32_t* d_rows, int32_t per_query,

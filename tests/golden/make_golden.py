@@ -22,6 +22,14 @@ Fixtures:
                     results for 100 queries at tau 0.3/0.6/0.8, k_out=10.
   ref_int.idx       the kernels_int.npz hierarchy written by the reference's
                     save_index (GGNN v1 bytes, index_file.py:55-91).
+  latent20k.npz     reference build of latent16 (SURVEY 8d G_B) 20k x 128 with
+                    BuildConfig(seed=7); query() ids for 2000 fresh queries at
+                    tau 0.3 / 0.45 / 0.6 (GPU-built vs reference-built recall,
+                    the north star's 0.5-point bar).
+  gist3k.npz        float latent16 (d = 960, the C3 "GIST-like" generator)
+                    3000 x 960: reference graph + query() results (float parity).
+  deep3k.npz        gen_synthetic clustered d = 96, rows L2-normalised (the C4
+                    "Deep-like" generator) 3000 x 96: reference graph + results.
   sharded_int.npz   reference build_sharded of the kernels_int data
                     (shard_size 250 -> 3 shards), every shard's graph, the
                     permutation, and query_sharded results (ids, dists,
@@ -192,12 +200,53 @@ def make_index_and_sharded(R):
     print("ref_int.idx", (OUT / "ref_int.idx").stat().st_size, "bytes; sharded_int.npz", len(si.shards), "shards")
 
 
+def deep_like(n, m, d=96, seed=1234):
+    """C4 generator (SURVEY 8d): gen_synthetic clustered, rows L2-normalised;
+    the last m rows are the held-out queries."""
+    from paper_1912_01059_b200.data import gen_synthetic
+
+    X = gen_synthetic(n + m, d, seed=seed, law="clustered", clusters=64).vectors.astype(np.float64)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    X = X.astype(np.float32)
+    return X[:n].copy(), X[n:].copy()
+
+
+def make_float_shapes(R):
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    for name, (base, queries) in (("gist3k", make_latent16(n=3000, d=960, m=200, seed=1234, as_float=True)),
+                                  ("deep3k", deep_like(3000, 200))):
+        sha = hashlib.sha256(base.tobytes() + queries.tobytes()).hexdigest()
+        h, stats = R.build(R.Dataset(base.copy()), R.BuildConfig(seed=7))
+        out = {"data_sha256": np.array(sha), "build_seconds_ref": np.float64(stats.build_seconds)}
+        out.update({k: v for k, v in graph_arrays(h).items() if not k.startswith("nnd")})
+        ids, dists, cnt = query_table(R, h, queries, R.QueryConfig(k_out=10, tau=0.6))
+        out["q_ids"], out["q_dists"], out["q_cnt"] = ids, dists, cnt
+        np.savez_compressed(OUT / f"{name}.npz", **out)
+        print(name, "build", stats.build_seconds, "s")
+
+
+def make_latent20k(R):
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, queries = make_latent16(n=20000, d=128, m=2000, seed=1234)
+    sha = hashlib.sha256(base.tobytes() + queries.tobytes()).hexdigest()
+    h, stats = R.build(R.Dataset(base.copy()), R.BuildConfig(seed=7))
+    out = {"data_sha256": np.array(sha), "build_seconds_ref": np.float64(stats.build_seconds)}
+    for tau in (0.3, 0.45, 0.6):
+        ids, dists, cnt = query_table(R, h, queries, R.QueryConfig(k_out=10, tau=tau))
+        t = f"{int(round(tau * 100)):03d}"
+        out[f"q{t}_ids"], out[f"q{t}_cnt"] = ids, cnt[:, :3]
+    np.savez_compressed(OUT / "latent20k.npz", **out)
+    print("latent20k build", stats.build_seconds, "s")
+
+
 def main():
     R = O.reference_module()
     if R is None:
         raise SystemExit("run oracle/build_ref.sh first (needs /root/reference)")
     assert R.backend.BACKEND == "compiled"
-    which = sys.argv[1:] or ["int", "float", "sift", "index"]
+    which = sys.argv[1:] or ["int", "float", "sift", "index", "shapes", "latent20k"]
     if "int" in which:
         make_kernels_int(R)
     if "float" in which:
@@ -206,6 +255,10 @@ def main():
         make_sift10k(R)
     if "index" in which:
         make_index_and_sharded(R)
+    if "shapes" in which:
+        make_float_shapes(R)
+    if "latent20k" in which:
+        make_latent20k(R)
 
 
 if __name__ == "__main__":

@@ -197,3 +197,30 @@ def test_shard_group_real_kernels_two_ranks():
         np.testing.assert_array_equal(cnt, ref.counters)
         np.testing.assert_array_equal(gi, gt.ids)
         np.testing.assert_array_equal(gd, gt.dists)
+
+
+@pytest.mark.parametrize("d,hi,k", [(32, 4, 10), (128, 256, 1), (128, 256, 32), (96, 256, 7), (224, 16, 12)])
+def test_bruteforce_tensor_cores_vs_checker(d, hi, k):
+    """tcgen05 kind::i8 exhaustive top-k (ggnn_exhaustive_topk_tc): ids and
+    distances equal the reference's exhaustive_topk (CPU checker, ties by row)
+    on uint8 data with many distance ties; n and m not multiples of the tiles."""
+    from paper_1912_01059_b200.device import DeviceVectors
+
+    rng = np.random.default_rng(d * 7 + k)
+    n, m = 5003, 301
+    X = rng.integers(0, hi, size=(n, d)).astype(np.float32)
+    X.setflags(write=False)
+    Q = rng.integers(0, hi, size=(m, d)).astype(np.float32)
+    dv = DeviceVectors.of_array(X)
+    dq, qs = dv.queries(Q)
+    t = N.torch()
+    ids = N.empty((m, k), t.int32)
+    dists = N.empty((m, k), t.float64)
+    N.call("ggnn_exhaustive_topk_tc", N.ctypes.byref(dv.struct), N.ctypes.byref(qs), k, N.ptr(ids), N.ptr(dists),
+           N.stream_ptr())
+    ids, dists = ids.cpu().numpy(), dists.cpu().numpy()
+    assert N.load().ggnn_bf_timeouts() == 0
+    for i in range(m):
+        ri, rd = O.exhaustive_topk(X, Q[i], k)
+        np.testing.assert_array_equal(ids[i], ri)
+        np.testing.assert_array_equal(dists[i], rd)
