@@ -60,6 +60,14 @@ int ggnn_merge_rows(int64_t node_count, int32_t k, int32_t k_nn, int32_t *d_adj,
                     double *d_dnn1, const int32_t *d_hit_ids, const double *d_hit_dists, int32_t hits_per_node,
                     int32_t *d_resc_ids, double *d_resc_dists, int32_t *d_changed, void *stream);
 
+/* ggnn_merge_rows for nodes node_begin .. node_begin + count - 1 only: hit
+ * and rescued rows are indexed from 0 (row i belongs to node node_begin + i).
+ * merge_layer applies its merges window by window with this (see build.py). */
+int ggnn_merge_rows_range(int64_t node_begin, int64_t count, int32_t k, int32_t k_nn, int32_t *d_adj, double *d_nnd,
+                          int32_t *d_sym_count, double *d_dnn1, const int32_t *d_hit_ids, const double *d_hit_dists,
+                          int32_t hits_per_node, int32_t *d_resc_ids, double *d_resc_dists, int32_t *d_changed,
+                          void *stream);
+
 /* Replaces: the check half of symmetrize (build.py:200-266 with
  * sym_check_pair, _core.pyx:375-435) for every (x, z) of a layer: pair
  * p = x * per_node + t checks direct slot t < k_nn of x, or rescued entry

@@ -276,7 +276,8 @@ bool leaf_tc_eligible(const ggnn_vectors* X, int64_t max_batch) {
 // the rest kept); displaced former neighbours go to the rescued list in their
 // former order -- AdjacencyLayer.merge_hits (graph.py:121-165).
 struct MergeArgs {
-  int64_t nc;
+  int64_t nc;             // rows in this launch: nodes x0 .. x0 + nc - 1
+  int64_t x0;
   int k, k_nn;
   int32_t* adj;
   double* nnd;
@@ -291,8 +292,9 @@ struct MergeArgs {
 };
 
 __global__ void __launch_bounds__(256) merge_rows_kernel(const __grid_constant__ MergeArgs a) {
-  const int64_t x = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (x >= a.nc) return;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= a.nc) return;
+  const int64_t x = a.x0 + i;  // node; hits and rescued rows are indexed by i
   const int lane = lane_id();
   const int k_nn = a.k_nn, k = a.k;
   int32_t* row = a.adj + x * k;
@@ -300,15 +302,15 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(const __grid_constant__
   double cd = lane < k_nn ? a.nnd[x * k_nn + lane] : 0.0;
   const int ncur = __popc(__ballot_sync(FULL, lane < k_nn && cid >= 0));  // direct slots are a prefix
   if (lane >= ncur) cid = -1;
-  int hid = lane < a.nh ? a.hit_id[x * a.nh + lane] : -1;
-  double hd = lane < a.nh ? a.hit_d[x * a.nh + lane] : 0.0;
+  int hid = lane < a.nh ? a.hit_id[i * a.nh + lane] : -1;
+  double hd = lane < a.nh ? a.hit_d[i * a.nh + lane] : 0.0;
   bool hv = hid >= 0 && hid != (int)x;
   for (int i = 0; i < ncur; ++i) {
     const int c = __shfl_sync(FULL, cid, i);  // every lane shuffles (no short-circuit)
     hv = hv && hid != c;
   }
   const int nextra = __popc(__ballot_sync(FULL, hv));
-  int32_t* rid = a.resc_id + x * k_nn;
+  int32_t* rid = a.resc_id + i * k_nn;
   if (nextra == 0) {
     if (lane < k_nn) rid[lane] = -1;
     return;
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(const __grid_constant__
   __syncwarp();
   if (evicted) {
     rid[erank] = cid;
-    a.resc_d[x * k_nn + erank] = cd;
+    a.resc_d[i * k_nn + erank] = cd;
   }
   // inverse slots: drop ids that became direct, keep the order of the rest
   const int ns = a.symc[x];
@@ -604,9 +606,23 @@ int ggnn_merge_rows(int64_t node_count, int32_t k, int32_t k_nn, int32_t* d_adj,
   GGNN_CHECK_ARG(k >= 1 && k <= MAX_K && k_nn >= 1 && k_nn <= k && hits_per_node >= 0 && hits_per_node <= 32,
                  "invalid merge geometry");
   if (node_count <= 0) return GGNN_OK;
-  MergeArgs a{node_count, k, k_nn, d_adj, d_nnd, d_sym_count, d_dnn1, d_hit_ids, d_hit_dists, hits_per_node,
+  return ggnn_merge_rows_range(0, node_count, k, k_nn, d_adj, d_nnd, d_sym_count, d_dnn1, d_hit_ids, d_hit_dists,
+                               hits_per_node, d_resc_ids, d_resc_dists, d_changed, stream);
+}
+
+int ggnn_merge_rows_range(int64_t node_begin, int64_t count, int32_t k, int32_t k_nn, int32_t* d_adj, double* d_nnd,
+                          int32_t* d_sym_count, double* d_dnn1, const int32_t* d_hit_ids, const double* d_hit_dists,
+                          int32_t hits_per_node, int32_t* d_resc_ids, double* d_resc_dists, int32_t* d_changed,
+                          void* stream) {
+  GGNN_CHECK_ARG(d_adj && d_nnd && d_sym_count && d_dnn1 && d_hit_ids && d_hit_dists && d_resc_ids && d_resc_dists,
+                 "invalid arguments");
+  GGNN_CHECK_ARG(node_begin >= 0 && k >= 1 && k <= MAX_K && k_nn >= 1 && k_nn <= k && hits_per_node >= 0 &&
+                     hits_per_node <= 32,
+                 "invalid merge geometry");
+  if (count <= 0) return GGNN_OK;
+  MergeArgs a{count, node_begin, k, k_nn, d_adj, d_nnd, d_sym_count, d_dnn1, d_hit_ids, d_hit_dists, hits_per_node,
               d_resc_ids, d_resc_dists, d_changed};
-  merge_rows_kernel<<<(unsigned)((node_count + 7) / 8), 256, 0, as_stream(stream)>>>(a);
+  merge_rows_kernel<<<(unsigned)((count + 7) / 8), 256, 0, as_stream(stream)>>>(a);
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
