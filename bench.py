@@ -44,9 +44,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ggnn", choices=["ggnn", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--d", type=int, default=None)
     ap.add_argument("--queries", type=int, default=10_000)
+    ap.add_argument("--workload", default="sift1m", choices=["sift1m", "gist1m", "deep10m"],
+                    help="sift1m = configs[1] (the metric's workload, default); gist1m / deep10m = the C3 / C4 "
+                         "shapes on one GPU (ground truth on a query subsample)")
+    ap.add_argument("--gt-queries", type=int, default=None, help="ground-truth subsample (default: all for sift1m, "
+                    "1000 otherwise)")
     ap.add_argument("--tau", type=float, default=None, help="skip the sweep and use this tau")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -148,11 +153,28 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ data
+WORKLOADS = {
+    "sift1m": "SIFT1M-shaped latent16 (SURVEY.md 8d G_B) {n}x{d} integer-valued (uint8 on the device)",
+    "gist1m": "GIST1M-shaped float latent16 {n}x{d} (C3: no rounding, /255)",
+    "deep10m": "Deep10M-shaped {n}x{d} clustered (1024 clusters), rows L2-normalised (C4)",
+}
+
+
 def make_workload(args):
+    """(base, queries) of the chosen workload; sizes default to the config's."""
     from paper_1912_01059_b200.synthetic import make_latent16
 
-    base, queries = make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234)
-    return base, queries
+    if args.workload == "sift1m":
+        return make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234)
+    if args.workload == "gist1m":
+        return make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234, as_float=True)
+    from paper_1912_01059_b200.data import gen_synthetic
+
+    X = gen_synthetic(args.n + args.queries, args.d, seed=1234, law="clustered", clusters=1024).vectors
+    X = X.astype(np.float64)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    X = X.astype(np.float32)
+    return X[:args.n].copy(), X[args.n:].copy()
 
 
 def recall_at(ids, gt_first, k):
@@ -271,8 +293,14 @@ def cpu_reference_qps(root: Path, nq_total: int, target_seconds: float, max_proc
 
 
 # ------------------------------------------------------------------ main
+DEFAULT_SHAPE = {"sift1m": (1_000_000, 128), "gist1m": (1_000_000, 960), "deep10m": (10_000_000, 96)}
+
+
 def main():
     args = parse()
+    n0, d0 = DEFAULT_SHAPE[args.workload]
+    args.n = args.n or n0
+    args.d = args.d or d0
     import torch
 
     dist = Dist(torch, args.gpus)
@@ -293,9 +321,10 @@ def main():
 
     torch.cuda.synchronize()
     t_gt = time.perf_counter()
-    gt_ids, _ = ga.search.exact_knn(ds, Q, 10)  # tcgen05 brute force (exact u8 distances)
+    gt_m = args.gt_queries or (Q.shape[0] if args.workload == "sift1m" else min(1000, Q.shape[0]))
+    gt_ids, _ = ga.search.exact_knn(ds, Q[:gt_m], 10)  # tcgen05 brute force for uint8 data
     gt_s = time.perf_counter() - t_gt
-    chosen, sweep = choose_tau(ga, h, Q, gt_ids, args.tau)
+    chosen, sweep = choose_tau(ga, h, Q[:gt_m], gt_ids, args.tau)
     tau = chosen["tau"]
     qcfg = ga.QueryConfig(k_out=10, tau=tau)
 
@@ -393,15 +422,18 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8" if dv.exact_integers else "f32",
-        "data": "synthetic latent16 (SURVEY.md 8d G_B), seed 1234",
-        "config": {"workload": f"SIFT1M-shaped latent16 {args.n}x{args.d}, {m} queries/rank, k=10, k_build=24",
+        "data": f"synthetic, seed 1234: {WORKLOADS[args.workload].format(n=args.n, d=args.d)}",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload].format(n=args.n, d=args.d)}, "
+                               f"{m} queries/rank, k=10, k_build=24",
+                   "recall_queries": gt_m,
                    "tau": tau, "recall": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
                    "mean_visited": chosen["V"], "mean_steps": chosen["T"], "tau_sweep": sweep,
                    "build_seconds": build_s, "ground_truth_seconds": gt_s,
                    "build_phase_seconds_top": dict(sorted(
                        bstats.phase_seconds.items(), key=lambda kv: -kv[1])[:6]),
                    "parallelism": f"replicas x{args.gpus} (independent query batches)",
-                   "l2": "inputs larger than L2 (u8 vectors 128 MB + adjacency 96 MB)"},
+                   "l2": f"inputs larger than L2 (vectors {base.nbytes // (4 if dv.exact_integers else 1) >> 20} MB "
+                         f"+ adjacency {args.n * 96 >> 20} MB on the device)"},
         "build_seconds": build_s,
         "e2e": e2e,
         "gpu_launches": args.steps,
