@@ -421,7 +421,10 @@ struct RefTable {
     if (s >= 0 && lane_id() == 0) t[s] = TOMB;
     __syncwarp();
   }
-  // per-lane tombstoning of a live key with count 1 (distinct keys per lane)
+  // per-lane tombstoning of a live key with count 1 (distinct keys per lane).
+  // A lane probing past another lane's slot may read it before or after that
+  // lane writes TOMB; either value is "occupied, not my key", so the probe
+  // continues the same way (racecheck reports this as a benign WAR warning).
   __device__ __forceinline__ void tomb_lane(uint32_t key) {
     uint32_t s = home(key);
     for (;;) {

@@ -125,6 +125,9 @@ struct WarpSearch {
   // adjacency row of the predicted next expansion, loaded while the current
   // step merges (pf_nb: this lane's slot of row pf_node)
   int pf_node, pf_nb;
+  // ring position of the next expansion when known from the last merge
+  // (-1: none left), -2 when head() must scan
+  int next_head;
   int visited, steps, distinct, forgotten, term;
   bool found_target;
 
@@ -174,6 +177,7 @@ struct WarpSearch {
     rebuild_at = (int)((ht.mask + 1) * 3 / 4);
     pf_node = -1;
     pf_nb = -1;
+    next_head = -2;
     visited = steps = distinct = forgotten = 0;
     term = TERM_EMPTY;
     found_target = false;
@@ -291,7 +295,9 @@ struct WarpSearch {
 
   // Lanes [0, m) hold ascending, distinct, currently-unknown (key, id) pairs.
   // Equivalent to calling the reference's _ring_insert on each in order.
-  __device__ void merge(Key key, int id, int m) {
+  // Returns the first unvisited ring position after the merge, given q = the
+  // first unvisited position before it (-1 if none; q == -2: unknown).
+  __device__ int merge(Key key, int id, int m, int q = -2) {
     const int lane = lane_id();
     int rank = 0;
     if (lane < m) {
@@ -321,9 +327,16 @@ struct WarpSearch {
     const bool ok = lane < m && p < c.cap;
     const int madm = __popc(__ballot_sync(FULL, ok));
     forgotten += m - madm;  // worse than the tail of a full ring
-    if (madm == 0) return;
+    if (madm == 0) return q;
     const int newL = min(c.cap, L + madm);
     const int E = L + madm - newL;
+    // next expansion: the first admitted candidate or the old q, shifted by
+    // the candidates placed before it (q is gone if it was evicted)
+    int nh = -2;
+    if (q != -2) {
+      nh = __shfl_sync(FULL, p, 0);
+      if (q >= 0 && q < L - E) nh = min(nh, q + __popc(__ballot_sync(FULL, ok && rank <= q)));
+    }
     if (E > 0) evict(E);
     // Scatter the merged sequence in place, top chunk first: output position
     // o holds the candidate whose slot is o, else ring entry o - #{candidates
@@ -377,6 +390,7 @@ struct WarpSearch {
     L = newL;
     __syncwarp();
     if (used > rebuild_at) rebuild();
+    return nh;
   }
 
   // Seeds: lanes [0, n) hold (key, id) in the caller's order; duplicates and
@@ -396,12 +410,13 @@ struct WarpSearch {
     else distinct += cnt;
     warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n)
     if (cnt) merge(key, id, cnt);
+    next_head = -2;
   }
 
   // One expansion.  Returns false when the search has terminated.
   __device__ bool step() {
     const int lane = lane_id();
-    const int pos = head();
+    const int pos = next_head != -2 ? next_head : head();
     if (pos < 0) {
       term = TERM_EMPTY;
       return false;
@@ -477,10 +492,13 @@ struct WarpSearch {
       // predict the next expansion -- the smaller of the next unvisited ring
       // entry and the best admitted candidate -- and load its adjacency row
       // while the merge runs (checked against the real head next step)
-      if (!found) prefetch_next(pos, m > 0, KO::shfl(key, 0), __shfl_sync(FULL, id, 0));
-      if (m) merge(key, id, m);
+      const int q = head_from(pos + 1);
+      if (!found) prefetch_next(q, m > 0, KO::shfl(key, 0), __shfl_sync(FULL, id, 0));
+      next_head = m ? merge(key, id, m, q) : q;
     } else {
-      prefetch_next(pos, false, KO::max_key(), INT_MAX);
+      const int q = head_from(pos + 1);
+      prefetch_next(q, false, KO::max_key(), INT_MAX);
+      next_head = q;
     }
     steps++;
     if (found) {
@@ -491,8 +509,8 @@ struct WarpSearch {
     return true;
   }
 
-  __device__ __forceinline__ void prefetch_next(int pos, bool have_cand, Key kc, int ic) {
-    const int q = head_from(pos + 1);
+  // q = first unvisited ring position after the one being expanded (-1: none)
+  __device__ __forceinline__ void prefetch_next(int q, bool have_cand, Key kc, int ic) {
     Key ko = KO::max_key();
     int io = INT_MAX;
     if (q >= 0) {
