@@ -123,6 +123,13 @@ class _Staging:
 _STAGING: dict = {}
 
 
+# host-to-host batches are cut into this many chunks, alternating over two
+# streams: chunk i+1's host copy and upload overlap chunk i's search, and
+# chunk i's results come back while later chunks still search
+_CHUNKS = int(__import__("os").environ.get("GGNN_E2E_CHUNKS", "2"))
+_STREAMS: dict = {}
+
+
 def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     t = N.torch()
     dv = dh.vectors
@@ -130,25 +137,55 @@ def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     k = cfg.k_out
     dev = t.cuda.current_device()
     st = _STAGING.setdefault(dev, _Staging()).ensure(m, d, k)
-    stream = t.cuda.current_stream()
-    np.copyto(st.q_pin[:m].numpy(), Q)
-    st.q_f32[:m].copy_(st.q_pin[:m], non_blocking=True)
-    qs = N.queries_struct(data=st.q_f32, dtype_code=N.GGNN_F32, m=m)
-    if dv.exact_integers:
-        st.flag.fill_(1)
-        N.call("ggnn_f32_to_u8", N.ptr(st.q_f32), m * d, N.ptr(st.q_u8), N.ptr(st.flag), N.stream_ptr())
-        st.flag_pin.copy_(st.flag, non_blocking=True)
-        stream.synchronize()
-        if int(st.flag_pin[0]) == 1:
-            qs = N.queries_struct(data=st.q_u8, dtype_code=N.GGNN_U8, m=m)
+    streams = _STREAMS.get(dev)
+    if streams is None:
+        streams = _STREAMS[dev] = (t.cuda.Stream(), t.cuda.Stream())
+    main = t.cuda.current_stream()
     params = _params(cfg, _flags(dv, False))
-    N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct), N.ptr(dh.top_rows),
-           dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, N.ptr(st.ids), N.ptr(st.dists),
-           N.ptr(st.cnt), None, 0, N.stream_ptr())
-    st.ids_pin[:m].copy_(st.ids[:m], non_blocking=True)
-    st.dists_pin[:m].copy_(st.dists[:m], non_blocking=True)
-    st.cnt_pin[:m].copy_(st.cnt[:m], non_blocking=True)
-    stream.synchronize()
+    nchunks = max(1, min(_CHUNKS, m // 1024))
+    bounds = [m * i // nchunks for i in range(nchunks + 1)]
+    narrow = dv.exact_integers
+    if narrow:
+        st.flag.fill_(1)
+    for s in streams:
+        s.wait_stream(main)
+    for c in range(nchunks):
+        lo, hi = bounds[c], bounds[c + 1]
+        s = streams[c & 1]
+        np.copyto(st.q_pin[lo:hi].numpy(), Q[lo:hi])
+        with t.cuda.stream(s):
+            sp = N.P(s.cuda_stream)
+            st.q_f32[lo:hi].copy_(st.q_pin[lo:hi], non_blocking=True)
+            if narrow:  # uint8 queries when every value is an integer in [0, 255]
+                N.call("ggnn_f32_to_u8", N.ptr(st.q_f32[lo:hi]), (hi - lo) * d, N.ptr(st.q_u8[lo:hi]),
+                       N.ptr(st.flag), sp)
+                qs = N.queries_struct(data=st.q_u8[lo:hi], dtype_code=N.GGNN_U8, m=hi - lo)
+            else:
+                qs = N.queries_struct(data=st.q_f32[lo:hi], dtype_code=N.GGNN_F32, m=hi - lo)
+            N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
+                   N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max,
+                   N.ptr(st.ids[lo:hi]), N.ptr(st.dists[lo:hi]), N.ptr(st.cnt[lo:hi]), None, 0, sp)
+            st.ids_pin[lo:hi].copy_(st.ids[lo:hi], non_blocking=True)
+            st.dists_pin[lo:hi].copy_(st.dists[lo:hi], non_blocking=True)
+            st.cnt_pin[lo:hi].copy_(st.cnt[lo:hi], non_blocking=True)
+    if narrow:
+        with t.cuda.stream(streams[(nchunks - 1) & 1]):
+            streams[(nchunks - 1) & 1].wait_stream(streams[nchunks & 1])
+            st.flag_pin.copy_(st.flag, non_blocking=True)
+    for s in streams:
+        main.wait_stream(s)
+    main.synchronize()
+    if narrow and int(st.flag_pin[0]) != 1:
+        # some query is not integral: the uint8 searches above are void; search
+        # the float batch (already on the device) against the uint8 table
+        qs = N.queries_struct(data=st.q_f32, dtype_code=N.GGNN_F32, m=m)
+        N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
+               N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max,
+               N.ptr(st.ids), N.ptr(st.dists), N.ptr(st.cnt), None, 0, N.stream_ptr())
+        st.ids_pin[:m].copy_(st.ids[:m], non_blocking=True)
+        st.dists_pin[:m].copy_(st.dists[:m], non_blocking=True)
+        st.cnt_pin[:m].copy_(st.cnt[:m], non_blocking=True)
+        main.synchronize()
     return BatchResult(st.ids_pin[:m].numpy().copy(), st.dists_pin[:m].numpy().copy(),
                        st.cnt_pin[:m].numpy().copy())
 
