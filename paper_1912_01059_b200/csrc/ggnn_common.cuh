@@ -82,19 +82,21 @@ __device__ __forceinline__ uint64_t pack_ki(uint32_t key, int id) {
   return ((uint64_t)key << 32) | (uint64_t)(uint32_t)id;
 }
 
-// Bitonic sort of the first `width` (16 or 32) lanes, ascending; for width 16
-// lanes 16..31 must hold values >= every lane below (the padding).
-__device__ __forceinline__ void warp_sort_u64(uint64_t& v, int width) {
+// Bitonic sort of the first W (16 or 32) lanes, ascending, fully unrolled;
+// for W = 16 lanes 16..31 must hold values >= every lane below (padding).
+template <int W>
+__device__ __forceinline__ void warp_sort_u64(uint64_t& v) {
   const int lane = lane_id();
-  for (int size = 2; size <= width; size <<= 1) {
 #pragma unroll
-    for (int stride = 16; stride > 0; stride >>= 1) {
-      if (stride >= size) continue;
+  for (int size = 2; size <= W; size <<= 1) {
+    const bool up = ((lane & size) == 0);
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
       const uint64_t o = __shfl_xor_sync(FULL, v, stride);
-      const bool up = ((lane & size) == 0);
       const bool lower = ((lane & stride) == 0);
       // lower lane of an ascending pair keeps the min, of a descending pair the max
-      v = (lower == up) ? (o < v ? o : v) : (o > v ? o : v);
+      const bool take = (lower == up) ? (o < v) : (o > v);
+      v = take ? o : v;
     }
   }
 }
@@ -104,7 +106,10 @@ template <typename K>
 __device__ __forceinline__ void warp_sort_n(K& key, int& id, int n) {
   if constexpr (sizeof(K) == 4) {
     uint64_t v = pack_ki(key, id);
-    warp_sort_u64(v, n <= 16 ? 16 : 32);
+    if (n <= 16)
+      warp_sort_u64<16>(v);
+    else
+      warp_sort_u64<32>(v);
     key = (K)(v >> 32);
     id = (int)(uint32_t)v;
   } else {
