@@ -188,6 +188,7 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
         if (rp[u]) acc[u] += part_f32(v[u], qc);
+      if constexpr (LPR < 32) break;  // at most one chunk per lane (see dists_u8_vec)
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -216,6 +217,8 @@ __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const 
       rp[u] = r >= 0 ? reinterpret_cast<const uint4*>(X + (int64_t)r * d) : nullptr;
       acc[u] = 0u;
     }
+    // choose_lpr picks the smallest power of two >= the chunk count (capped
+    // at 32), so below 32 lanes per row every lane owns at most one chunk
     for (int c = sub; c < nch; c += LPR) {
       uint4 v[UNR];
       const uint4 qv = reinterpret_cast<const uint4*>(qs)[c];
@@ -225,6 +228,7 @@ __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const 
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
         if (rp[u]) acc[u] += part_u8(v[u], qv);
+      if constexpr (LPR < 32) break;
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
