@@ -9,7 +9,17 @@ hand-written sm_100a kernels in libggnn_b200.so behind a C ABI
 
 from . import backend
 from .config import BuildConfig, QueryConfig
-from .data import ConfigError, Dataset, FormatError, gen_synthetic, squared_distance
+from .data import (
+    ConfigError,
+    Dataset,
+    FormatError,
+    gen_synthetic,
+    load_ids,
+    load_vectors,
+    squared_distance,
+    write_ids,
+    write_vectors,
+)
 from .graph import SENTINEL, AdjacencyLayer, GraphStats, Hierarchy
 from .search import (
     BatchResult,

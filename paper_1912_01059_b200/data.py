@@ -84,3 +84,71 @@ def gen_synthetic(n: int, d: int, seed: int, law: str = "uniform", clusters: int
     else:
         raise ValueError(f"unknown law {law!r}")
     return Dataset(arr)
+
+
+# ------------------------------------------------------------- TexMex files
+# fvecs / bvecs / ivecs: every record is a little-endian int32 dimension
+# followed by that many float32 / uint8 / int32 values (data.py:80-160 in the
+# reference).  Host utilities: parsed with one reshape of the raw bytes.
+_ELEM = {"fvecs": np.dtype("<f4"), "bvecs": np.dtype("u1"), "ivecs": np.dtype("<i4")}
+
+
+def _records(path, kind: str) -> np.ndarray:
+    raw = np.fromfile(path, dtype=np.uint8)
+    if raw.size < 4:
+        raise FormatError(f"{path}: no records (file has {raw.size} bytes)")
+    d = int(raw[:4].view("<i4")[0])
+    if d <= 0:
+        raise FormatError(f"{path}: invalid dimension {d} at byte offset 0")
+    esz = _ELEM[kind].itemsize
+    rec = 4 + d * esz
+    n, tail = divmod(raw.size, rec)
+    if tail:
+        raise FormatError(f"{path}: truncated {kind} file, {tail} trailing bytes after {n} records of {rec} bytes "
+                          f"(byte offset {n * rec})")
+    table = raw.reshape(n, rec)
+    dims = np.ascontiguousarray(table[:, :4]).view("<i4").ravel()
+    if (dims != d).any():
+        bad = int(np.argmax(dims != d))
+        raise FormatError(f"{path}: inconsistent dimension, record {bad} claims {int(dims[bad])} (expected {d}, "
+                          f"byte offset {bad * rec})")
+    return np.ascontiguousarray(table[:, 4:]).view(_ELEM[kind]).reshape(n, d)
+
+
+def load_vectors(path, fmt: str = "fvecs") -> Dataset:
+    """fvecs or bvecs file -> Dataset (bvecs bytes promoted to float32)."""
+    if fmt not in ("fvecs", "bvecs"):
+        raise ValueError(f"unknown vector format {fmt!r} (expected 'fvecs' or 'bvecs')")
+    arr = _records(path, fmt).astype(np.float32)
+    if fmt == "fvecs":
+        finite = np.isfinite(arr).all(axis=1)
+        if not finite.all():
+            raise FormatError(f"{path}: non-finite value in record {int(np.argmin(finite))}")
+    return Dataset(arr)
+
+
+def load_ids(path) -> np.ndarray:
+    """ivecs id table -> (m, k) int32."""
+    arr = _records(path, "ivecs").astype(np.int32)
+    if (arr < 0).any():
+        r, c = np.argwhere(arr < 0)[0]
+        raise FormatError(f"{path}: negative index {int(arr[r, c])} in record {int(r)}")
+    return arr
+
+
+def _write(path, body: np.ndarray, kind: str) -> None:
+    n, d = body.shape
+    out = np.empty((n, 4 + d * _ELEM[kind].itemsize), dtype=np.uint8)
+    out[:, :4] = np.full((n, 1), d, dtype="<i4").view(np.uint8)
+    out[:, 4:] = np.ascontiguousarray(body.astype(_ELEM[kind])).view(np.uint8).reshape(n, -1)
+    out.tofile(path)
+
+
+def write_vectors(path, vectors: np.ndarray, fmt: str = "fvecs") -> None:
+    if fmt not in ("fvecs", "bvecs"):
+        raise ValueError(f"unknown vector format {fmt!r}")
+    _write(path, np.asarray(vectors), fmt)
+
+
+def write_ids(path, ids: np.ndarray) -> None:
+    _write(path, np.asarray(ids), "ivecs")

@@ -93,3 +93,27 @@ def test_oracle_shard_merge_matches_reference():
         np.testing.assert_array_equal(gi, g["q_ids"][i, :nh])
         np.testing.assert_array_equal(gd, g["q_dists"][i, :nh])
         assert (v, t, term) == tuple(int(c) for c in g["q_cnt"][i])
+
+
+def test_texmex_io_round_trip_and_reference_bytes(tmp_path):
+    """fvecs / bvecs / ivecs files: byte-identical to the reference's writers
+    and readable by its readers (when the compiled reference is present)."""
+    rng = np.random.default_rng(3)
+    X = rng.integers(0, 256, size=(7, 5)).astype(np.float32)
+    ids = rng.integers(0, 100, size=(4, 3)).astype(np.int32)
+    ga.write_vectors(tmp_path / "a.fvecs", X)
+    ga.write_vectors(tmp_path / "a.bvecs", X, fmt="bvecs")
+    ga.write_ids(tmp_path / "a.ivecs", ids)
+    np.testing.assert_array_equal(ga.load_vectors(tmp_path / "a.fvecs").vectors, X)
+    np.testing.assert_array_equal(ga.load_vectors(tmp_path / "a.bvecs", fmt="bvecs").vectors, X)
+    np.testing.assert_array_equal(ga.load_ids(tmp_path / "a.ivecs"), ids)
+    (tmp_path / "bad.fvecs").write_bytes((tmp_path / "a.fvecs").read_bytes()[:-3])
+    with pytest.raises(ga.FormatError):
+        ga.load_vectors(tmp_path / "bad.fvecs")
+    R = O.reference_module()
+    if R is not None:
+        R.write_vectors(tmp_path / "r.fvecs", X)
+        R.write_vectors(tmp_path / "r.bvecs", X, fmt="bvecs")
+        R.write_ids(tmp_path / "r.ivecs", ids)
+        for ext in ("fvecs", "bvecs", "ivecs"):
+            assert (tmp_path / f"r.{ext}").read_bytes() == (tmp_path / f"a.{ext}").read_bytes()
