@@ -29,9 +29,21 @@ SYM_CHECK_VISITED = 128
 SYM_FALLBACK = 8
 # node windows per symmetrize pass: requests of x-window w are re-checked after the
 # claims of windows < w, approximating the reference's sequential x order
-SYM_WINDOWS = int(__import__("os").environ.get("GGNN_SYM_WINDOWS", "16"))
-# node windows per merge pass (see _merge_pass)
-MERGE_WINDOWS = int(__import__("os").environ.get("GGNN_MERGE_WINDOWS", "16"))
+# Node windows per symmetrize / merge pass: the reference walks the nodes of a
+# pass in order and every node sees the links earlier nodes created; windows
+# approximate that order (later windows see earlier windows' updates).  Small
+# layers take fine windows (cheap, and where single links matter most:
+# tests/golden/deep3k); large layers 16 (each window still fills the GPU).
+SMALL_LAYER = 20_000
+_ENV = __import__("os").environ
+
+
+def _sym_windows(nc: int) -> int:
+    return int(_ENV.get("GGNN_SYM_WINDOWS", 128 if nc <= SMALL_LAYER else 16))
+
+
+def _merge_windows(nc: int) -> int:
+    return int(_ENV.get("GGNN_MERGE_WINDOWS", 64 if nc <= SMALL_LAYER else 16))
 CONSENSUS_SAMPLE = 256
 CONSENSUS_K = 10
 
@@ -213,9 +225,9 @@ def _merge_pass(h, j: int):
     # snapshot pass loses that: on strongly clustered data it measurably
     # weakens cross-cluster navigation (reference with a snapshot merge:
     # R@10 0.93 vs 0.98 on tests/golden/deep3k).  Descents therefore run in
-    # MERGE_WINDOWS consecutive node windows, each applied before the next
-    # descends (16 windows reproduce the sequential result there).
-    windows = max(1, min(MERGE_WINDOWS, nc))
+    # consecutive node windows (_merge_windows), each applied before the next
+    # descends.
+    windows = max(1, min(_merge_windows(nc), nc))
     for w in range(windows):
         lo, hi = nc * w // windows, nc * (w + 1) // windows
         if hi <= lo:
@@ -268,7 +280,7 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
         ws.tgt[:cnt].fill_(-1)
         ws.dropped.zero_()
         nc = layer.node_count
-        windows = max(1, min(SYM_WINDOWS, cnt))
+        windows = max(1, min(_sym_windows(nc), cnt))
         while True:
             x_end = nc if rounds >= windows else (nc * (rounds + 1) + windows - 1) // windows
             if rounds:
