@@ -101,10 +101,33 @@ __device__ __forceinline__ void warp_sort_u64(uint64_t& v) {
   }
 }
 
+// Rank sort of distinct packed words: lanes [0, n) hold the values (lanes >= n
+// padding that is never smaller); every valid lane counts the smaller values
+// with n independent broadcasts (no dependent chain, unlike a bitonic
+// network) and scatters itself through `scratch` (32 u64, shared).
+__device__ __forceinline__ void warp_rank_sort_u64(uint64_t& v, int n, uint64_t* scratch) {
+  const int lane = lane_id();
+  int rank = 0;
+  for (int j = 0; j < n; ++j) rank += (__shfl_sync(FULL, v, j) < v) ? 1 : 0;
+  __syncwarp();
+  if (lane < n) scratch[rank] = v;
+  __syncwarp();
+  if (lane < n) v = scratch[lane];
+  __syncwarp();
+}
+
 // Sort of the first n (<= 32) (key, id) lanes, padding (max, INT_MAX) above n.
+// With a scratch buffer, exact integer keys use the rank sort above.
 template <typename K>
-__device__ __forceinline__ void warp_sort_n(K& key, int& id, int n) {
+__device__ __forceinline__ void warp_sort_n(K& key, int& id, int n, uint64_t* scratch = nullptr) {
   if constexpr (sizeof(K) == 4) {
+    if (scratch) {
+      uint64_t v = pack_ki(key, id);
+      warp_rank_sort_u64(v, n, scratch);
+      key = (K)(v >> 32);
+      id = (int)(uint32_t)v;
+      return;
+    }
     uint64_t v = pack_ki(key, id);
     if (n <= 16)
       warp_sort_u64<16>(v);

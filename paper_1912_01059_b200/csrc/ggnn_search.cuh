@@ -408,7 +408,7 @@ struct WarpSearch {
     const int cnt = __popc(__ballot_sync(FULL, v));
     if (ever) distinct += warp_sum(ever_insert(v ? id : -1));
     else distinct += cnt;
-    warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n)
+    warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n): bitonic
     if (cnt) merge(key, id, cnt);
     next_head = -2;
   }
@@ -484,7 +484,8 @@ struct WarpSearch {
       __syncwarp();
       visited += nc;
       if (ever) distinct += warp_sum(ever_insert(lane < nc ? id : -1));
-      warp_sort_n(key, id, nc);
+      // candidates are compacted into lanes [0, nc); crow / cid are free now
+      warp_sort_n(key, id, nc, reinterpret_cast<uint64_t*>(crow));
       const bool adm = lane < nc && KO::to_d(key) <= thr;
       const int m = __popc(__ballot_sync(FULL, adm));
       forgotten += nc - m;

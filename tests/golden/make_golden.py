@@ -30,6 +30,10 @@ Fixtures:
                     3000 x 960: reference graph + query() results (float parity).
   deep3k.npz        gen_synthetic clustered d = 96, rows L2-normalised (the C4
                     "Deep-like" generator) 3000 x 96: reference graph + results.
+  deep100k.npz      the C4 generator (gen_synthetic clustered, 1024 clusters,
+                    rows L2-normalised) at 100k x 96 + 1000 held-out queries:
+                    query() ids of the reference-built graph at tau 0.3 / 0.6
+                    / 1.0 / 2.0 (medium-scale build parity on clustered data).
   sharded_int.npz   reference build_sharded of the kernels_int data
                     (shard_size 250 -> 3 shards), every shard's graph, the
                     permutation, and query_sharded results (ids, dists,
@@ -241,6 +245,29 @@ def make_latent20k(R):
     print("latent20k build", stats.build_seconds, "s")
 
 
+def deep_c4(n, m, d=96, seed=1234):
+    """C4 generator at size n (1024 clusters as in bench.py --workload deep10m)."""
+    from paper_1912_01059_b200.data import gen_synthetic
+
+    X = gen_synthetic(n + m, d, seed=seed, law="clustered", clusters=1024).vectors.astype(np.float64)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    X = X.astype(np.float32)
+    return X[:n].copy(), X[n:].copy()
+
+
+def make_deep100k(R):
+    base, queries = deep_c4(100_000, 1000)
+    sha = hashlib.sha256(base.tobytes() + queries.tobytes()).hexdigest()
+    h, stats = R.build(R.Dataset(base.copy()), R.BuildConfig(seed=7))
+    out = {"data_sha256": np.array(sha), "build_seconds_ref": np.float64(stats.build_seconds)}
+    for tau in (0.3, 0.6, 1.0, 2.0):
+        ids, dists, cnt = query_table(R, h, queries, R.QueryConfig(k_out=10, tau=tau))
+        t = f"{int(round(tau * 100)):03d}"
+        out[f"q{t}_ids"], out[f"q{t}_cnt"] = ids, cnt[:, :3]
+    np.savez_compressed(OUT / "deep100k.npz", **out)
+    print("deep100k build", stats.build_seconds, "s")
+
+
 def main():
     R = O.reference_module()
     if R is None:
@@ -259,6 +286,8 @@ def main():
         make_float_shapes(R)
     if "latent20k" in which:
         make_latent20k(R)
+    if "deep100k" in which:
+        make_deep100k(R)
 
 
 if __name__ == "__main__":
