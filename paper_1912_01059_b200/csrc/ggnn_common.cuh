@@ -152,6 +152,18 @@ template <> struct VecTraits<uint8_t, uint8_t> { using Key = uint32_t; };
 template <> struct VecTraits<uint8_t, float> { using Key = double; };
 
 // Partial distance of the elements [e0, e0+CH) handled by one lane.
+// FP32 partial: the lane's share of a float row summed in single precision
+// (rounding ~1e-7 relative, far inside the north star's 1e-5 near-tie band);
+// the group reduction and everything after it stay FP64, and returned hits
+// are re-scored with the exact sequential FP64 sum (FLAG_EXACT_DISTS).
+__device__ __forceinline__ float part_f32_sp(const float4 a, const float* q) {
+  const float d0 = a.x - q[0], d1 = a.y - q[1], d2 = a.z - q[2], d3 = a.w - q[3];
+  return fmaf(d3, d3, fmaf(d2, d2, fmaf(d1, d1, d0 * d0)));
+}
+#ifndef GGNN_F32_PARTIALS
+#define GGNN_F32_PARTIALS 1
+#endif
+
 __device__ __forceinline__ double part_f32(const float4 a, const float* q) {
   double d0 = (double)a.x - (double)q[0], d1 = (double)a.y - (double)q[1];
   double d2 = (double)a.z - (double)q[2], d3 = (double)a.w - (double)q[3];
@@ -202,6 +214,9 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
       rp[u] = r >= 0 ? reinterpret_cast<const float4*>(X + (int64_t)r * d) : nullptr;
       acc[u] = 0.0;
     }
+    float accf[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) accf[u] = 0.0f;
     for (int c = sub; c < nch; c += LPR) {
       float4 v[UNR];
 #pragma unroll
@@ -209,9 +224,16 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
         if (rp[u]) v[u] = __ldg(rp[u] + c);
       const float* qc = qs + 4 * c;
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (rp[u]) acc[u] += part_f32(v[u], qc);
+      for (int u = 0; u < UNR; ++u) {
+        if (!rp[u]) continue;
+        if constexpr (GGNN_F32_PARTIALS) accf[u] += part_f32_sp(v[u], qc);
+        else acc[u] += part_f32(v[u], qc);
+      }
       if constexpr (LPR < 32) break;  // at most one chunk per lane (see dists_u8_vec)
+    }
+    if constexpr (GGNN_F32_PARTIALS) {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) acc[u] = (double)accf[u];
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
