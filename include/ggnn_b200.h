@@ -150,9 +150,10 @@ int ggnn_exhaustive_topk(const ggnn_vectors *X, const int32_t *d_rows, int64_t n
 /* Same contract as ggnn_exhaustive_topk over the whole table, forced onto the
  * tcgen05 path (kind::i8 MMA of 128-query tiles against streamed 256-row
  * tiles, exact integer distances, top-k epilogue from TMEM); GGNN_E_INVALID
- * unless X and Q are uint8, d % 32 == 0, d <= 224, 1 <= k <= 32.
- * ggnn_exhaustive_topk takes this path by itself for such whole-table scans
- * of at least 4096 rows. */
+ * unless X and Q are uint8, d % 32 == 0, and 1 <= k <= 32 with d <= 224 or
+ * 32 < k <= 128 with d <= 128.  ggnn_exhaustive_topk takes this path by
+ * itself for such whole-table scans of at least 4096 rows (and is limited to
+ * k <= 32 otherwise). */
 int ggnn_exhaustive_topk_tc(const ggnn_vectors *X, const ggnn_queries *Q, int32_t k, int32_t *d_ids,
                             double *d_dists, void *stream);
 

@@ -28,8 +28,11 @@ namespace {
 
 constexpr int BF_M = 128;        // queries per CTA (TMEM lanes)
 constexpr int BF_N = 256;        // X rows per tile (accumulator columns)
-constexpr int BF_THREADS = 256;  // 8 warps: lane quarter = warp & 3, column half = warp >> 2
-constexpr int BF_TOPSTRIDE = 33;
+// k <= 32: 8 warps, lane quarter = warp & 3, column half = warp >> 2 (two
+// partial lists per query); 32 < k <= 128: 4 warps, one list per query
+// (the per-thread lists of k packed words then fill the shared memory).
+constexpr int BF_K_SMALL = 32;
+constexpr int BF_K_MAX = 128;
 
 struct BfArgs {
   const uint8_t* X;
@@ -69,12 +72,14 @@ __global__ void sqnorm_u8_kernel(const uint8_t* X, int64_t n, int d, uint32_t* o
   out[i] = s;
 }
 
-inline size_t bf_smem(int d) {
-  return (size_t)BF_M * d + 2 * (size_t)BF_N * d + 3 * BF_N * 4 + BF_M * 4 +
-         (size_t)BF_THREADS * BF_TOPSTRIDE * 8 + 32;
+inline size_t bf_smem(int d, int k, int threads) {
+  return (size_t)BF_M * d + 2 * (size_t)BF_N * d + 3 * BF_N * 4 + BF_M * 4 + (size_t)threads * (k + 1) * 8 + 32;
 }
 
-__global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_constant__ BfArgs a) {
+template <int HALVES>
+__global__ void __launch_bounds__(128 * HALVES, 1) bf_tc_kernel(const __grid_constant__ BfArgs a) {
+  constexpr int THREADS = 128 * HALVES;
+  constexpr int COLS = BF_N / HALVES;  // columns scanned per thread and tile
   extern __shared__ __align__(16) uint8_t smem_bf[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.d, nch = K >> 4;
@@ -87,7 +92,8 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
   uint32_t* xn = reinterpret_cast<uint32_t*>(B + 2 * (size_t)BF_N * K);  // three stages of BF_N
   uint32_t* qn = xn + 3 * BF_N;
   uint64_t* top = reinterpret_cast<uint64_t*>(qn + BF_M);
-  uint64_t* mbar = top + (size_t)BF_THREADS * BF_TOPSTRIDE;
+  const int tstride = a.k + 1;
+  uint64_t* mbar = top + (size_t)THREADS * tstride;
   uint32_t* taddr = reinterpret_cast<uint32_t*>(mbar + 2);
 
   if (warp == 0) tc::tmem_alloc<512>(taddr);
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
     tc::mbar_init(&mbar[1], 1);
   }
   // query tile (rows past m are zero) and its norms
-  for (int t = tid; t < BF_M * nch; t += BF_THREADS) {
+  for (int t = tid; t < BF_M * nch; t += THREADS) {
     const int r = t / nch, c = t - r * nch;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     if (q0 + r < a.m) {
@@ -105,21 +111,21 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
     }
     *reinterpret_cast<uint4*>(A + tc::il_offset(r, c * 16, K)) = v;
   }
-  uint64_t* mytop = top + (size_t)tid * BF_TOPSTRIDE;
+  uint64_t* mytop = top + (size_t)tid * tstride;
   for (int j = 0; j < a.k; ++j) mytop[j] = ~0ull;
   uint64_t kth = ~0ull;
 
   auto load_tile = [&](int64_t t, int stage) {
     const uint32_t bs = tc::smem_u32(B + (size_t)stage * BF_N * K);
     const int64_t r0 = t * BF_N;
-    for (int e = tid; e < BF_N * nch; e += BF_THREADS) {
+    for (int e = tid; e < BF_N * nch; e += THREADS) {
       const int r = e / nch, c = e - r * nch;
       const bool valid = r0 + r < a.n;
       const uint8_t* src = a.X + (valid ? (r0 + r) : 0) * (int64_t)K + c * 16;
       cp_async16(bs + tc::il_offset(r, c * 16, K), src, valid);
     }
     const uint32_t ns = tc::smem_u32(xn + (t % 3) * BF_N);
-    for (int r = tid; r < BF_N / 4; r += BF_THREADS) {
+    for (int r = tid; r < BF_N / 4; r += THREADS) {
       const bool valid = r0 + 4 * r + 3 < a.n;
       if (valid) {
         cp_async16(ns + r * 16, a.xnorm + r0 + 4 * r, true);
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
   const uint32_t tmem = *taddr;
   const uint32_t idesc = tc::idesc_u8(BF_M, BF_N);
   const uint32_t sbo = (uint32_t)nch * 128u;
-  const int wq = warp & 3, half = warp >> 2;
+  const int wq = warp & 3, half = HALVES == 2 ? (warp >> 2) : 0;
   const int row = wq * 32 + lane;
   const uint32_t qnr = qn[row];
   uint32_t phase[2] = {0u, 0u};
@@ -159,13 +165,13 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
   auto epilogue = [&](int64_t t, int stage) {
     const uint32_t* xs = xn + (t % 3) * BF_N;
     const int64_t r0 = t * BF_N;
-    const uint32_t base = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(stage * BF_N + half * (BF_N / 2));
-    for (int c0 = 0; c0 < BF_N / 2; c0 += 16) {
+    const uint32_t base = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(stage * BF_N + half * COLS);
+    for (int c0 = 0; c0 < COLS; c0 += 16) {
       uint32_t v[16];
       tc::tmem_ld16(base + (uint32_t)c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int col = half * (BF_N / 2) + c0 + j;
+        const int col = half * COLS + c0 + j;
         const int64_t id = r0 + col;
         const uint32_t dist = qnr + xs[col] - 2u * v[j];
         const uint64_t pk = ((uint64_t)dist << 32) | (uint64_t)(uint32_t)id;
@@ -217,9 +223,9 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
     epilogue(t_end - 1, ls);
   }
   if (!ok && lane == 0) atomicAdd(&g_bf_timeouts, 1);
-  // this thread's partial top-k -> block (2 * sp + half)
+  // this thread's partial top-k -> block (HALVES * sp + half)
   if (q0 + row < a.m) {
-    uint8_t* blk = a.blocks + (size_t)(2 * sp + half) * a.block_bytes;
+    uint8_t* blk = a.blocks + (size_t)(HALVES * sp + half) * a.block_bytes;
     int32_t* ids = reinterpret_cast<int32_t*>(blk) + (q0 + row) * a.k;
     double* ds = reinterpret_cast<double*>(blk + a.dists_off) + (q0 + row) * a.k;
     for (int j = 0; j < a.k; ++j) {
@@ -233,13 +239,44 @@ __global__ void __launch_bounds__(BF_THREADS, 1) bf_tc_kernel(const __grid_const
   if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
+// k-way merge of G ascending (dist, id) lists per query (k > 32 path of the
+// brute force; ggnn_shard_merge covers k <= 32).  One thread per query.
+__global__ void merge_lists_kernel(const uint8_t* blocks, size_t block_bytes, size_t dists_off, int G, int64_t m,
+                                   int k, int32_t* out_ids, double* out_dists) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  int head[16];
+  for (int g = 0; g < G; ++g) head[g] = 0;
+  for (int j = 0; j < k; ++j) {
+    int best = -1;
+    double bd = 0.0;
+    int bi = INT_MAX;
+    for (int g = 0; g < G; ++g) {
+      if (head[g] >= k) continue;
+      const uint8_t* blk = blocks + (size_t)g * block_bytes;
+      const int32_t id = reinterpret_cast<const int32_t*>(blk)[q * k + head[g]];
+      if (id < 0) continue;
+      const double dd = reinterpret_cast<const double*>(blk + dists_off)[q * k + head[g]];
+      if (best < 0 || dd < bd || (dd == bd && id < bi)) {
+        best = g;
+        bd = dd;
+        bi = id;
+      }
+    }
+    out_ids[q * k + j] = best < 0 ? -1 : bi;
+    out_dists[q * k + j] = best < 0 ? __longlong_as_double(0x7ff0000000000000ll) : bd;
+    if (best >= 0) ++head[best];
+  }
+}
+
 }  // namespace
 
 // true when the tensor-core path applies to this scan
 bool bf_tc_eligible(const ggnn_vectors* X, const int32_t* d_rows, const ggnn_queries* Q, int k) {
   const int qd = Q->d_rows ? X->dtype : Q->dtype;
-  return X->dtype == GGNN_U8 && qd == GGNN_U8 && d_rows == nullptr && k >= 1 && k <= 32 && X->d % 32 == 0 &&
-         X->d <= 224 && X->n < INT32_MAX && (reinterpret_cast<uintptr_t>(X->d_data) & 15) == 0 &&
+  const int dmax = k <= BF_K_SMALL ? 224 : 128;
+  return X->dtype == GGNN_U8 && qd == GGNN_U8 && d_rows == nullptr && k >= 1 && k <= BF_K_MAX && X->d % 32 == 0 &&
+         X->d <= dmax && X->n < INT32_MAX && (reinterpret_cast<uintptr_t>(X->d_data) & 15) == 0 &&
          (Q->d_rows || (reinterpret_cast<uintptr_t>(Q->d_data) & 15) == 0);
 }
 
@@ -250,16 +287,18 @@ int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_i
   DevInfo di = dev_info();
   const int64_t qtiles = (m + BF_M - 1) / BF_M;
   const int64_t tiles = (n + BF_N - 1) / BF_N;
+  const int halves = k <= BF_K_SMALL ? 2 : 1;
   int64_t splits = std::max<int64_t>(1, (2 * (int64_t)std::max(di.sm_count, 1) + qtiles - 1) / qtiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, tiles / 4));
+  if (halves == 1) splits = std::min<int64_t>(splits, 16);  // merge_lists_kernel keeps 16 list heads
   const int64_t per = (tiles + splits - 1) / splits;
   splits = (tiles + per - 1) / per;
   const size_t bb = ggnn_shard_block_bytes(m, k);
   uint8_t* blocks = nullptr;
   uint32_t* xnorm = nullptr;
-  GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&blocks), bb * 2 * splits, st));
+  GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&blocks), bb * halves * splits, st));
   GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&xnorm), (size_t)n * 4, st));
-  GGNN_CUDA_TRY(cudaMemsetAsync(blocks, 0, bb * 2 * splits, st));
+  GGNN_CUDA_TRY(cudaMemsetAsync(blocks, 0, bb * halves * splits, st));
   const uint8_t* Xd = static_cast<const uint8_t*>(X->d_data);
   sqnorm_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Xd, n, X->d, xnorm);
   GGNN_LAUNCH_CHECK();
@@ -278,11 +317,21 @@ int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_i
   a.blocks = blocks;
   a.block_bytes = bb;
   a.dists_off = ggnn_shard_block_dists_offset(m, k);
-  const size_t smem = bf_smem(X->d);
-  GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  bf_tc_kernel<<<(unsigned)(qtiles * splits), BF_THREADS, smem, st>>>(a);
-  GGNN_LAUNCH_CHECK();
-  int rc = ggnn_shard_merge(blocks, (int32_t)(2 * splits), m, k, k, d_ids, d_dists, nullptr, st);
+  const size_t smem = bf_smem(X->d, k, 128 * halves);
+  int rc = GGNN_OK;
+  if (halves == 2) {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bf_tc_kernel<2><<<(unsigned)(qtiles * splits), 256, smem, st>>>(a);
+    GGNN_LAUNCH_CHECK();
+    rc = ggnn_shard_merge(blocks, (int32_t)(2 * splits), m, k, k, d_ids, d_dists, nullptr, st);
+  } else {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bf_tc_kernel<1><<<(unsigned)(qtiles * splits), 128, smem, st>>>(a);
+    GGNN_LAUNCH_CHECK();
+    merge_lists_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(blocks, bb, a.dists_off, (int)splits, m, k,
+                                                                     d_ids, d_dists);
+    GGNN_LAUNCH_CHECK();
+  }
   cudaFreeAsync(blocks, st);
   cudaFreeAsync(xnorm, st);
   return rc;

@@ -998,7 +998,8 @@ int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const i
 
 int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t nrows, const ggnn_queries* Q,
                          int32_t k, int32_t* d_ids, double* d_dists, void* stream) {
-  ggnn_search_params p{k, 1, 1, 0, 0.0, 0};
+  GGNN_CHECK_ARG(k >= 1, "k must be >= 1 (got %d)", k);
+  ggnn_search_params p{std::min(k, 32), 1, 1, 0, 0.0, 0};
   SearchArgs a;
   int rc = fill_common(a, X, Q, &p);
   if (rc) return rc;
@@ -1006,6 +1007,8 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   // whole-table scans of uint8 data at least one X tile per split long: tensor cores
   if (bf_tc_eligible(X, d_rows, Q, k) && nrows == X->n && X->n >= 4096)
     return bf_topk_tc(X, Q, k, d_ids, d_dists, as_stream(stream));
+  GGNN_CHECK_ARG(k <= 32, "k must be <= 32 here (k <= 128 needs uint8 data with d %% 32 == 0, d <= 128, and at "
+                 "least 4096 rows); got %d", k);
   a.top_rows = d_rows;
   a.ntop = nrows;
   a.ids = d_ids;
@@ -1029,12 +1032,14 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
 
 int ggnn_exhaustive_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int32_t k, int32_t* d_ids,
                             double* d_dists, void* stream) {
-  ggnn_search_params p{k, 1, 1, 0, 0.0, 0};
+  GGNN_CHECK_ARG(k >= 1, "k must be >= 1 (got %d)", k);
+  ggnn_search_params p{std::min(k, 32), 1, 1, 0, 0.0, 0};
   SearchArgs a;
   int rc = fill_common(a, X, Q, &p);
   if (rc) return rc;
   GGNN_CHECK_ARG(bf_tc_eligible(X, nullptr, Q, k),
-                 "the tensor-core scan needs uint8 table and queries, d %% 32 == 0, d <= 224, k in [1, 32]");
+                 "the tensor-core scan needs uint8 table and queries, d %% 32 == 0, and k <= 32 with d <= 224 "
+                 "or k <= 128 with d <= 128");
   return bf_topk_tc(X, Q, k, d_ids, d_dists, as_stream(stream));
 }
 

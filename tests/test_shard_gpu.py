@@ -224,3 +224,20 @@ def test_bruteforce_tensor_cores_vs_checker(d, hi, k):
         ri, rd = O.exhaustive_topk(X, Q[i], k)
         np.testing.assert_array_equal(ids[i], ri)
         np.testing.assert_array_equal(dists[i], rd)
+
+
+@pytest.mark.parametrize("k", [33, 100, 128])
+def test_bruteforce_tensor_cores_large_k(k):
+    """k > 32 (the reference CLI's gt default is 100): one list per query in the
+    tensor-core kernel, then a k-way merge of the split lists."""
+    rng = np.random.default_rng(k)
+    n, m, d = 9001, 130, 64
+    X = rng.integers(0, 8, size=(n, d)).astype(np.float32)
+    Q = rng.integers(0, 8, size=(m, d)).astype(np.float32)
+    gt = ga.brute_force_oracle(ga.Dataset(X), Q, k)
+    for i in range(0, m, 7):
+        ri, rd = O.exhaustive_topk(X, Q[i], k)
+        np.testing.assert_array_equal(gt.ids[i], ri)
+        np.testing.assert_array_equal(gt.dists[i], rd)
+    with pytest.raises(ValueError):
+        ga.brute_force_oracle(ga.Dataset(X[:1000]), Q, 40)  # below the tensor-core size: k <= 32 only
