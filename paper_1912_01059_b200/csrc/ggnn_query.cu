@@ -727,7 +727,7 @@ int fill_common(SearchArgs& a, const ggnn_vectors* X, const ggnn_queries* Q, con
   a.m = Q->m;
   a.c = make_cfg(p);
   int keysize = (X->dtype == GGNN_U8 && qd == GGNN_U8) ? 4 : 8;
-  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(qd), keysize);
+  a.region = set_layout(a.c, X->d, qelem_of(qd), keysize);
   return GGNN_OK;
 }
 
@@ -930,7 +930,7 @@ int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const d
   a.req_count = d_req_count;
   a.req_cap = req_cap;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
-  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
+  a.region = set_layout(a.c, X->d, qelem_of(X->dtype), keysize);
   cudaStream_t st = as_stream(stream);
   if (X->dtype == GGNN_U8) return launch_sym<uint8_t>(a, npairs, st);
   return launch_sym<float>(a, npairs, st);
@@ -959,7 +959,7 @@ int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_
   a.stage = d_stage;
   a.x_end = x_end;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
-  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
+  a.region = set_layout(a.c, X->d, qelem_of(X->dtype), keysize);
   cudaStream_t st = as_stream(stream);
   if (X->dtype == GGNN_U8) return launch_sym<uint8_t>(a, nreq, st);
   return launch_sym<float>(a, nreq, st);
@@ -990,7 +990,7 @@ int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const i
   a.verdict = d_verdict;
   a.fallback = d_fallback;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
-  a.region = warp_region_bytes(a.c.cap, a.c.vsz, a.c.hlog, X->d, qelem_of(X->dtype), keysize);
+  a.region = set_layout(a.c, X->d, qelem_of(X->dtype), keysize);
   cudaStream_t st = as_stream(stream);
   if (X->dtype == GGNN_U8) return launch_sym<uint8_t>(a, npairs, st);
   return launch_sym<float>(a, npairs, st);

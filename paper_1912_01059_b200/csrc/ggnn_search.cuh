@@ -33,6 +33,8 @@ struct SearchCfg {
   double tau;
   long long max_steps;  // max_iterations, or the budget in found-target mode
   int flags;
+  // byte offsets of the per-warp shared region (set_layout); the ring starts at 0
+  uint32_t o_rvis, o_vring, o_ht, o_crow, o_cid, o_ckey, o_qs;
 };
 
 constexpr int FLAG_DISTINCT = 1;     // exact distinct_touched via a global set
@@ -56,16 +58,26 @@ __host__ __device__ inline bool vring_local(int vsz) { return vsz <= 32 * VR_SLO
   int vring_lane_[VR_SLOTS > 0 ? VR_SLOTS : 1]; \
   (s).vr = vring_lane_
 
-// Byte size of one warp's shared region.
-inline size_t warp_region_bytes(int cap, int vsz, int hlog, int64_t d, int qelem, int keysize) {
-  size_t b = 0;
-  b += align16((size_t)cap * keysize);      // rk
-  b += align16((size_t)cap * 4);            // rid
-  b += align16((size_t)((cap + 127) / 128) * 128);  // rvis (padded for 4-byte scans)
-  if (!vring_local(vsz)) b += align16((size_t)vsz * 4);  // vring (shared only when large)
-  b += align16((size_t)(1u << hlog) * 4);   // ht
-  b += 32 * 4 + 32 * 4 + align16(32 * (size_t)keysize);  // crow, cid, ckey
-  b += align16((size_t)d * qelem);          // qs
+// Lay out one warp's shared region (offsets into c, computed once on the
+// host so the kernels address every array as base + constant) and return its
+// byte size: ring keys + ids (packed u64 words for 4-byte keys), visited
+// flags (padded for 4-byte scans), the shared visited ring when it is too
+// large for the lanes, the refcount table, candidate rows / ids / keys and
+// the query.
+inline size_t set_layout(SearchCfg& c, int64_t d, int qelem, int keysize) {
+  size_t b = align16((size_t)c.cap * keysize) + align16((size_t)c.cap * 4);
+  c.o_rvis = (uint32_t)b;
+  b += align16((size_t)((c.cap + 127) / 128) * 128);
+  c.o_vring = (uint32_t)b;
+  if (!vring_local(c.vsz)) b += align16((size_t)c.vsz * 4);
+  c.o_ht = (uint32_t)b;
+  b += align16((size_t)(1u << c.hlog) * 4);
+  c.o_crow = (uint32_t)b;
+  c.o_cid = (uint32_t)(b + 32 * 4);
+  c.o_ckey = (uint32_t)(b + 64 * 4);
+  b += 64 * 4 + align16(32 * (size_t)keysize);
+  c.o_qs = (uint32_t)b;
+  b += align16((size_t)d * qelem);
   return b;
 }
 
@@ -141,34 +153,21 @@ struct WarpSearch {
   }
 
   __device__ void carve(uint8_t* base) {
-    uint8_t* p = base;
     if constexpr (PACK) {
-      re = reinterpret_cast<uint64_t*>(p);
-      p += align16((size_t)c.cap * sizeof(Key)) + align16((size_t)c.cap * 4);
+      re = reinterpret_cast<uint64_t*>(base);
     } else {
-      rk = reinterpret_cast<Key*>(p);
-      p += align16((size_t)c.cap * sizeof(Key));
-      rid = reinterpret_cast<int*>(p);
-      p += align16((size_t)c.cap * 4);
+      rk = reinterpret_cast<Key*>(base);
+      rid = reinterpret_cast<int*>(base + align16((size_t)c.cap * sizeof(Key)));
     }
-    rvis = p;
-    p += align16((size_t)((c.cap + 127) / 128) * 128);
-    vring = nullptr;
-    if (!vring_local(c.vsz)) {
-      vring = reinterpret_cast<int*>(p);
-      p += align16((size_t)c.vsz * 4);
-    }
-    ht.t = reinterpret_cast<uint32_t*>(p);
+    rvis = base + c.o_rvis;
+    vring = vring_local(c.vsz) ? nullptr : reinterpret_cast<int*>(base + c.o_vring);
+    ht.t = reinterpret_cast<uint32_t*>(base + c.o_ht);
     ht.mask = (1u << c.hlog) - 1u;
     ht.shift = 32 - c.hlog;
-    p += align16((size_t)(1u << c.hlog) * 4);
-    crow = reinterpret_cast<int*>(p);
-    p += 32 * 4;
-    cid = reinterpret_cast<int*>(p);
-    p += 32 * 4;
-    ckey = reinterpret_cast<Key*>(p);
-    p += align16(32 * sizeof(Key));
-    qs = reinterpret_cast<TQ*>(p);
+    crow = reinterpret_cast<int*>(base + c.o_crow);
+    cid = reinterpret_cast<int*>(base + c.o_cid);
+    ckey = reinterpret_cast<Key*>(base + c.o_ckey);
+    qs = reinterpret_cast<TQ*>(base + c.o_qs);
   }
 
   __device__ void reset() {
@@ -386,7 +385,7 @@ struct WarpSearch {
       __syncwarp();
     }
     int took = ok ? ht.insert_new((uint32_t)id) : 0;
-    used += warp_sum(took);
+    used += __popc(__ballot_sync(FULL, took != 0));
     L = newL;
     __syncwarp();
     if (used > rebuild_at) rebuild();
@@ -406,7 +405,7 @@ struct WarpSearch {
       id = INT_MAX;
     }
     const int cnt = __popc(__ballot_sync(FULL, v));
-    if (ever) distinct += warp_sum(ever_insert(v ? id : -1));
+    if (ever) distinct += __popc(__ballot_sync(FULL, ever_insert(v ? id : -1) != 0));
     else distinct += cnt;
     warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n): bitonic
     if (cnt) merge(key, id, cnt);
@@ -483,7 +482,7 @@ struct WarpSearch {
       }
       __syncwarp();
       visited += nc;
-      if (ever) distinct += warp_sum(ever_insert(lane < nc ? id : -1));
+      if (ever) distinct += __popc(__ballot_sync(FULL, ever_insert(lane < nc ? id : -1) != 0));
       // candidates are compacted into lanes [0, nc); crow / cid are free now
       warp_sort_n(key, id, nc, reinterpret_cast<uint64_t*>(crow));
       const bool adm = lane < nc && KO::to_d(key) <= thr;
