@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--d", type=int, default=None)
     ap.add_argument("--queries", type=int, default=10_000)
-    ap.add_argument("--workload", default="sift1m", choices=["sift1m", "gist1m", "deep10m"],
+    ap.add_argument("--workload", default="sift1m", choices=["sift1m", "gist1m", "deep10m", "c5shard"],
                     help="sift1m = configs[1] (the metric's workload, default); gist1m / deep10m = the C3 / C4 "
                          "shapes on one GPU (ground truth on a query subsample)")
     ap.add_argument("--gt-queries", type=int, default=None, help="ground-truth subsample (default: all for sift1m, "
@@ -157,6 +157,7 @@ WORKLOADS = {
     "sift1m": "SIFT1M-shaped latent16 (SURVEY.md 8d G_B) {n}x{d} integer-valued (uint8 on the device)",
     "gist1m": "GIST1M-shaped float latent16 {n}x{d} (C3: no rounding, /255)",
     "deep10m": "Deep10M-shaped {n}x{d} clustered (1024 clusters), rows L2-normalised (C4)",
+    "c5shard": "one SIFT100M shard: latent16 {n}x{d} integer-valued (uint8 on the device; C5 is 8 such shards)",
 }
 
 
@@ -164,7 +165,7 @@ def make_workload(args):
     """(base, queries) of the chosen workload; sizes default to the config's."""
     from paper_1912_01059_b200.synthetic import make_latent16
 
-    if args.workload == "sift1m":
+    if args.workload in ("sift1m", "c5shard"):
         return make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234)
     if args.workload == "gist1m":
         return make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234, as_float=True)
@@ -293,7 +294,8 @@ def cpu_reference_qps(root: Path, nq_total: int, target_seconds: float, max_proc
 
 
 # ------------------------------------------------------------------ main
-DEFAULT_SHAPE = {"sift1m": (1_000_000, 128), "gist1m": (1_000_000, 960), "deep10m": (10_000_000, 96)}
+DEFAULT_SHAPE = {"sift1m": (1_000_000, 128), "gist1m": (1_000_000, 960), "deep10m": (10_000_000, 96),
+                 "c5shard": (12_500_000, 128)}
 
 
 def main():
