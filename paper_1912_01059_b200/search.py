@@ -91,11 +91,11 @@ def _check_query(h, q: np.ndarray) -> np.ndarray:
 
 
 class _Staging:
-    """Reusable pinned host / device buffers of the host-to-host query path
-    (one per device): the query batch goes host -> pinned -> device once as
-    float32, is narrowed to uint8 on the device when every value is an
-    integer in [0, 255] (ggnn_f32_to_u8), and the results come back through
-    pinned buffers -- no per-call allocations, one synchronisation."""
+    """Reusable device / pinned host buffers of the host-to-host query path
+    (one per device): the query batch is uploaded once as float32, narrowed
+    to uint8 on the device when every value is an integer in [0, 255]
+    (ggnn_f32_to_u8), and the results come back through pinned buffers -- no
+    per-call allocations, one synchronisation."""
 
     def __init__(self):
         self.m = self.d = self.k = 0
@@ -106,7 +106,6 @@ class _Staging:
         t = N.torch()
         m = max(m, self.m if (d == self.d and k == self.k) else 0)
         self.m, self.d, self.k = m, d, k
-        self.q_pin = t.empty((m, d), dtype=t.float32, pin_memory=True)
         self.ids_pin = t.empty((m, k), dtype=t.int32, pin_memory=True)
         self.dists_pin = t.empty((m, k), dtype=t.float64, pin_memory=True)
         self.cnt_pin = t.empty((m, 5), dtype=t.int32, pin_memory=True)
@@ -152,10 +151,12 @@ def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     for c in range(nchunks):
         lo, hi = bounds[c], bounds[c + 1]
         s = streams[c & 1]
-        np.copyto(st.q_pin[lo:hi].numpy(), Q[lo:hi])
         with t.cuda.stream(s):
             sp = N.P(s.cuda_stream)
-            st.q_f32[lo:hi].copy_(st.q_pin[lo:hi], non_blocking=True)
+            # straight from the caller's (pageable) array: the driver's staged
+            # copy beats a host copy into pinned memory plus a DMA (0.31 vs
+            # 0.41 ms for 10k x 128 float32, tools/hostreg_probe.py)
+            st.q_f32[lo:hi].copy_(t.from_numpy(Q[lo:hi]), non_blocking=True)
             if narrow:  # uint8 queries when every value is an integer in [0, 255]
                 N.call("ggnn_f32_to_u8", N.ptr(st.q_f32[lo:hi]), (hi - lo) * d, N.ptr(st.q_u8[lo:hi]),
                        N.ptr(st.flag), sp)

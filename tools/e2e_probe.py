@@ -30,7 +30,3 @@ for chunks in (1, 2, 3, 4, 1):
         ref = r.ids
     assert np.array_equal(r.ids, ref)
     print(f"chunks {chunks}: {dt * 1e3:.3f} ms per 10k -> {10000 / dt / 1e6:.3f} M QPS e2e")
-t0 = time.perf_counter()
-for _ in range(20):
-    np.copyto(search._STAGING[0].q_pin[:10000].numpy(), Q)
-print("host copy into pinned: %.3f ms" % ((time.perf_counter() - t0) / 20 * 1e3))
