@@ -95,7 +95,11 @@ int ggnn_version(void);
 /* Device properties used for sizing (SM count, smem per block). */
 int ggnn_device_info(int *sm_count, int *smem_per_block);
 
-/* Bytes of device workspace a search batch needs for the given flags. */
+/* Bytes of device workspace a search batch needs for the given flags.  With
+ * GGNN_FLAG_DISTINCT the default is a compact per-query set: a query that
+ * touches more ids than it holds reports distinct_touched = -1 and is rerun
+ * by the caller with the exact size, which max_seeds < 0 returns (a workspace
+ * that large always gets exact tables). */
 size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params *p, int32_t max_seeds);
 
 /* Replaces: AdjacencyLayer storage semantics read by _greedy_core

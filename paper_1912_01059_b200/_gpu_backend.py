@@ -120,15 +120,18 @@ def greedy_search(X, to_row, adj, k_nn, sym_count, q, seed_ids, seed_dists, k_ou
     flags = N.FLAG_DISTINCT | (0 if dv.exact_integers else N.FLAG_EXACT_DISTS)
     params = N.search_params(k_out, prioq_size, visited_size, tau, max_iterations, flags)
     t = N.torch()
-    nb = N.load().ggnn_search_workspace_bytes(1, ctypes.byref(params), seed_ids.shape[1])
-    ws = N.empty((max(nb, 1),), t.uint8)
     ids = N.empty((1, k_out), t.int32)
     dists = N.empty((1, k_out), t.float64)
     cnt = N.empty((1, 5), t.int32)
     sid, sd = N.to_dev(seed_ids), N.to_dev(seed_dists)
-    N.call("ggnn_greedy_batch", ctypes.byref(dv.struct), ctypes.byref(layer), ctypes.byref(qs), N.ptr(sid), N.ptr(sd),
-           seed_ids.shape[1], ctypes.byref(params), float(d_nn1_max), N.ptr(ids), N.ptr(dists), N.ptr(cnt),
-           N.ptr(ws), nb, N.stream_ptr())
+    for exact in (False, True):  # compact distinct-set first; exact on overflow (-1)
+        nb = N.load().ggnn_search_workspace_bytes(1, ctypes.byref(params), -1 if exact else seed_ids.shape[1])
+        ws = N.empty((max(nb, 1),), t.uint8)
+        N.call("ggnn_greedy_batch", ctypes.byref(dv.struct), ctypes.byref(layer), ctypes.byref(qs), N.ptr(sid),
+               N.ptr(sd), seed_ids.shape[1], ctypes.byref(params), float(d_nn1_max), N.ptr(ids), N.ptr(dists),
+               N.ptr(cnt), N.ptr(ws), nb, N.stream_ptr())
+        if int(cnt[0, 3].item()) >= 0:
+            break
     ids, dists, c = ids.cpu().numpy()[0], dists.cpu().numpy()[0], cnt.cpu().numpy()[0]
     nh = int((ids >= 0).sum())
     return ids[:nh].copy(), dists[:nh].copy(), int(c[0]), int(c[1]), int(c[2]), int(c[3]), int(c[4])

@@ -93,6 +93,7 @@ struct SearchArgs {
   int32_t* counters;
   uint32_t* ever;       // m * ever_size entries, or nullptr
   uint32_t ever_size;
+  int ever_cap;         // inserts allowed before a query reports overflow (INT_MAX: exact table)
   // query()
   const int32_t* top_rows;
   int64_t ntop;
@@ -155,6 +156,8 @@ __device__ __forceinline__ void init_search(WarpSearch<TX, TQ, LP>& s, const Sea
   s.carve(region);
   s.ever = a.ever ? a.ever + (size_t)qi * a.ever_size : nullptr;
   s.ever_mask = a.ever_size - 1u;
+  s.ever_cap = a.ever_cap;
+  s.ever_overflow = false;
 }
 
 template <typename TX, typename TQ, int LP>
@@ -202,7 +205,7 @@ __device__ void write_hits(const WarpSearch<TX, TQ, LP>& s, const SearchArgs& a,
     c[0] = s.visited + extra_visited;
     c[1] = s.steps;
     c[2] = s.term;
-    c[3] = s.distinct + extra_distinct;
+    c[3] = s.ever_overflow ? -1 : s.distinct + extra_distinct;  // -1: rerun with an exact table
     c[4] = s.forgotten;
   }
 }
@@ -312,6 +315,7 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
   int id = lane < kk ? bi + lo : -1;
   int nh = kk;
   int visited = hi - lo, steps = 0, distinct = (hi - lo) - kk, forgotten = 0, term = TERM_EMPTY;
+  bool ever_ovf = false;
   for (int j = a.start - 1; j >= a.stop; --j) {
     const LayerDev& Lj = a.layers[j];
     const int sid = lane < nh ? __ldg(a.layers[j + 1].down + id) : -1;
@@ -323,6 +327,7 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     visited += s.visited;
     steps += s.steps;
     distinct += s.distinct;
+    ever_ovf = ever_ovf || s.ever_overflow;
     forgotten += s.forgotten;
     term = s.term;
     nh = s.hits(bk, id);
@@ -348,7 +353,7 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     c[0] = visited;
     c[1] = steps;
     c[2] = term;
-    c[3] = distinct;
+    c[3] = ever_ovf ? -1 : distinct;
     c[4] = forgotten;
   }
 }
@@ -459,6 +464,8 @@ __device__ __forceinline__ void symcheck_kernel_one(const SymArgs& a, uint8_t* s
     s.carve(smem_w);
     s.ever = nullptr;
     s.ever_mask = 0;
+    s.ever_cap = INT_MAX;
+    s.ever_overflow = false;
     set_layer(s, a.layer);
     s.dmax = a.dmax;
     const int xrow = a.layer.to_row ? __ldg(a.layer.to_row + x) : x;
@@ -737,6 +744,15 @@ int combo(const ggnn_vectors* X, const ggnn_queries* Q) {
   return qd == GGNN_U8 ? 1 : 2;                // u8 / u8, u8 / f32
 }
 
+// Exact distinct_touched needs a per-query set of every id touched; a table
+// for the worst case (max_iterations * k touches) is 256 KB per query at the
+// defaults, while typical searches touch ~1-2 k ids.  ggnn_search_workspace_bytes
+// therefore asks for COMPACT_EVER entries per query; a query that fills 3/4 of
+// it stops counting and reports distinct_touched = -1, and the caller reruns
+// just those queries with a workspace of the exact size (attach_ever picks
+// the exact table whenever the workspace holds one).
+constexpr uint32_t COMPACT_EVER = 4096;
+
 uint32_t ever_size_for(const ggnn_search_params* p, int32_t max_seeds, int k) {
   uint64_t need = 2ull * ((uint64_t)max_seeds + (uint64_t)std::max<int64_t>(p->max_iterations, 1) * (uint64_t)k) + 64;
   uint32_t e = 64;
@@ -745,12 +761,18 @@ uint32_t ever_size_for(const ggnn_search_params* p, int32_t max_seeds, int k) {
 }
 
 int attach_ever(SearchArgs& a, const ggnn_search_params* p, int32_t max_seeds, int k, void* ws, size_t wsb) {
+  a.ever_cap = INT_MAX;
   if (!(p->flags & GGNN_FLAG_DISTINCT)) return GGNN_OK;
-  uint32_t e = ever_size_for(p, max_seeds, k);
-  size_t need = (size_t)a.m * e * 4;
-  GGNN_CHECK_ARG(ws != nullptr && wsb >= need, "GGNN_FLAG_DISTINCT needs %zu bytes of workspace", need);
+  const uint32_t full = ever_size_for(p, max_seeds, k);
+  const uint32_t small = std::min(full, COMPACT_EVER);
+  const size_t per = a.m > 0 ? wsb / ((size_t)a.m * 4) : 0;
+  GGNN_CHECK_ARG(ws != nullptr && per >= small, "GGNN_FLAG_DISTINCT needs %zu bytes of workspace (exact: %zu)",
+                 (size_t)a.m * small * 4, (size_t)a.m * full * 4);
+  uint32_t e = small;
+  while (e < full && (size_t)e * 2 <= per) e <<= 1;
   a.ever = reinterpret_cast<uint32_t*>(ws);
   a.ever_size = e;
+  a.ever_cap = e >= full ? INT_MAX : (int)(e / 4 * 3);
   return GGNN_OK;
 }
 
@@ -770,7 +792,10 @@ int ggnn_device_info(int* sm_count, int* smem_per_block) {
 
 size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params* p, int32_t max_seeds) {
   if (!p || !(p->flags & GGNN_FLAG_DISTINCT)) return 0;
-  return (size_t)m * ever_size_for(p, max_seeds, MAX_K) * 4;
+  // max_seeds < 0: room for the exact table of every query (any seed count <= 32)
+  const uint32_t full = ever_size_for(p, max_seeds < 0 ? 32 : max_seeds, MAX_K);
+  if (max_seeds < 0) return (size_t)m * full * 4;
+  return (size_t)m * std::min(full, COMPACT_EVER) * 4;
 }
 
 int ggnn_sanitize_layer(const int32_t* d_adj, const int32_t* d_sym_count, int64_t node_count, int32_t k,

@@ -129,9 +129,12 @@ struct WarpSearch {
   int* crow;
   int* cid;
   Key* ckey;
-  // diagnostic ever-set (global)
+  // diagnostic ever-set (global): the ids this search touched, for the exact
+  // distinct_touched; a compact table gives up (ever_overflow) past ever_cap
   uint32_t* ever;
   uint32_t ever_mask;
+  int ever_cap;
+  bool ever_overflow;
   // warp-uniform state
   int L, vlen, vpos, used, rebuild_at;
   // adjacency row of the predicted next expansion, loaded while the current
@@ -196,6 +199,13 @@ struct WarpSearch {
         continue;
       }
       s = (s + 1) & ever_mask;
+    }
+  }
+
+  __device__ __forceinline__ void check_ever() {
+    if (distinct > ever_cap) {  // compact table 3/4 full: stop, report -1
+      ever_overflow = true;
+      ever = nullptr;
     }
   }
 
@@ -405,7 +415,10 @@ struct WarpSearch {
       id = INT_MAX;
     }
     const int cnt = __popc(__ballot_sync(FULL, v));
-    if (ever) distinct += __popc(__ballot_sync(FULL, ever_insert(v ? id : -1) != 0));
+    if (ever) {
+      distinct += __popc(__ballot_sync(FULL, ever_insert(v ? id : -1) != 0));
+      check_ever();
+    }
     else distinct += cnt;
     warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n): bitonic
     if (cnt) merge(key, id, cnt);
@@ -482,7 +495,10 @@ struct WarpSearch {
       }
       __syncwarp();
       visited += nc;
-      if (ever) distinct += __popc(__ballot_sync(FULL, ever_insert(lane < nc ? id : -1) != 0));
+      if (ever) {
+        distinct += __popc(__ballot_sync(FULL, ever_insert(lane < nc ? id : -1) != 0));
+        check_ever();
+      }
       // candidates are compacted into lanes [0, nc); crow / cid are free now
       warp_sort_n(key, id, nc, reinterpret_cast<uint64_t*>(crow));
       const bool adm = lane < nc && KO::to_d(key) <= thr;

@@ -58,13 +58,13 @@ class BatchResult:
     counters: np.ndarray
 
     def results(self) -> list[QueryResult]:
-        out = []
-        for i in range(self.ids.shape[0]):
-            nh = int((self.ids[i] >= 0).sum())
-            c = self.counters[i]
-            out.append(QueryResult(self.ids[i, :nh].copy(), self.dists[i, :nh].copy(), int(c[0]), int(c[1]),
-                                   TERMINATED_BY[int(c[2])], int(c[3]), int(c[4])))
-        return out
+        """Per-query QueryResult objects; their id / distance arrays are views
+        of this batch's (private) host arrays, one row each."""
+        nh = (self.ids >= 0).sum(axis=1).tolist()
+        cnt = self.counters.tolist()
+        ids, dists = self.ids, self.dists
+        return [QueryResult(ids[i, :n], dists[i, :n], c[0], c[1], TERMINATED_BY[c[2]], c[3], c[4])
+                for i, (n, c) in enumerate(zip(nh, cnt))]
 
 
 def _params(cfg: QueryConfig, flags: int):
@@ -212,17 +212,29 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
     dists = N.empty((m, cfg.k_out), t.float64)
     cnt = N.empty((m, 5), t.int32)
     params = _params(cfg, _flags(dv, distinct))
-    chunk = _DISTINCT_CHUNK if distinct else max(m, 1)
     dq, qs = dv.queries(Q)
     bottom = dh.layers[0]
-    for lo in range(0, m, chunk):
-        hi = min(m, lo + chunk)
-        sub = N.Queries(N.P(dq.data_ptr() + lo * Q.shape[1] * dq.element_size()), None, hi - lo, qs.dtype, 0)
-        ws, wsb = _workspace(hi - lo, params, cfg.k_out)
+
+    def launch(rows_lo, rows_hi, sub_q, out_ids, out_d, out_c, exact):
+        ws, wsb = _workspace(rows_hi - rows_lo, params, -1 if exact else cfg.k_out)
         N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(bottom.struct), N.ptr(dh.top_rows),
-               dh.ntop, N.ctypes.byref(sub), N.ctypes.byref(params), dh.d_nn1_max, N.P(ids.data_ptr() + lo * 4 * cfg.k_out),
-               N.P(dists.data_ptr() + lo * 8 * cfg.k_out), N.P(cnt.data_ptr() + lo * 20), N.ptr(ws), wsb,
-               N.stream_ptr())
+               dh.ntop, N.ctypes.byref(sub_q), N.ctypes.byref(params), dh.d_nn1_max, out_ids, out_d, out_c,
+               N.ptr(ws), wsb, N.stream_ptr())
+
+    launch(0, m, qs, N.ptr(ids), N.ptr(dists), N.ptr(cnt), False)
+    if distinct and m:
+        # queries whose compact distinct-set overflowed (distinct_touched = -1)
+        # run again with exact per-query tables, a few at a time
+        redo = np.nonzero(cnt[:, 3].cpu().numpy() < 0)[0]
+        for lo in range(0, len(redo), _DISTINCT_CHUNK):
+            sel = redo[lo:lo + _DISTINCT_CHUNK]
+            sel_d = N.to_dev(sel.astype(np.int64))
+            dq2 = dq[sel_d].contiguous()
+            sub = N.Queries(N.ptr(dq2), None, len(sel), qs.dtype, 0)
+            i2, d2, c2 = N.empty((len(sel), cfg.k_out), t.int32), N.empty((len(sel), cfg.k_out), t.float64), \
+                N.empty((len(sel), 5), t.int32)
+            launch(0, len(sel), sub, N.ptr(i2), N.ptr(d2), N.ptr(c2), True)
+            ids[sel_d], dists[sel_d], cnt[sel_d] = i2, d2, c2
     if out == "device":
         return ids, dists, cnt
     return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())
@@ -335,10 +347,13 @@ def descent_arrays(h, queries, cfg: QueryConfig, start: int, stop: int, seg_lo=N
     dists = N.empty((m, cfg.k_out), t.float64)
     cnt = N.empty((m, 5), t.int32)
     params = _params(cfg, _flags(dv, distinct))
-    ws, wsb = _workspace(m, params, cfg.k_out)
-    N.call("ggnn_descent_batch", N.ctypes.byref(dv.struct), layers, dh.num_layers, start, stop, N.ctypes.byref(qs),
-           N.ptr(lo_d), N.ptr(hi_d), N.ctypes.byref(params), N.ptr(ids), N.ptr(dists), N.ptr(cnt), N.ptr(ws), wsb,
-           N.stream_ptr())
+    for exact in (False, True):
+        ws, wsb = _workspace(m, params, -1 if exact else cfg.k_out)
+        N.call("ggnn_descent_batch", N.ctypes.byref(dv.struct), layers, dh.num_layers, start, stop,
+               N.ctypes.byref(qs), N.ptr(lo_d), N.ptr(hi_d), N.ctypes.byref(params), N.ptr(ids), N.ptr(dists),
+               N.ptr(cnt), N.ptr(ws), wsb, N.stream_ptr())
+        if not distinct or not bool((cnt[:, 3] < 0).any()):
+            break  # (a compact distinct-set overflowed: rerun with exact tables)
     del keep
     return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())
 

@@ -204,3 +204,22 @@ def test_query_arrays_integral_and_fractional_queries(golden_sift):
             same += 1
             np.testing.assert_array_equal(b.dists[i, :len(dd)], dd)
     assert same >= 0.98 * len(Qf)
+
+
+def test_distinct_touched_exact_past_compact_table(golden_sift):
+    """Searches that touch more ids than the compact distinct-set holds
+    (3/4 of 4096) are rerun with exact tables: distinct_touched (and every
+    other counter) still equals the CPU checker's."""
+    g, h, queries = golden_sift
+    cfg = ga.QueryConfig(k_out=10, tau=1000.0, max_iterations=3000, prioq_size=2000, visited_size=2000)
+    res = ga.batch_query(h, queries[:40], cfg)
+    layers = [(L.adjacency, L.k_nn, L.sym_count) for L in h.layers]
+    X = h.dataset.vectors
+    big = 0
+    for i, r in enumerate(res):
+        ids, dd, v, t, term, distinct, forgotten = O.query(layers, h.to_bottom, X, queries[i], 10, 1000.0,
+                                                           h.stats.d_nn1_max, 3000, 2000, 2000)
+        assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten) == (
+            v, t, term, distinct, forgotten)
+        big += int(distinct > 3072)
+    assert big > 0  # the overflow path was exercised
