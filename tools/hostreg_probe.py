@@ -1,14 +1,9 @@
 """Cost of cudaHostRegister on a query batch vs a copy into pinned memory."""
-import ctypes
 import time
 
 import numpy as np
 import torch
 
-cudart = ctypes.CDLL("libcudart.so.12") if False else None
-import torch.cuda  # noqa: E402
-
-lib = ctypes.CDLL(torch.utils.cpp_extension.__file__ and "libcudart.so", mode=ctypes.RTLD_GLOBAL) if False else None
 Q = np.random.default_rng(0).random((10000, 128), dtype=np.float32)
 pin = torch.empty((10000, 128), dtype=torch.float32, pin_memory=True)
 dev = torch.empty((10000, 128), dtype=torch.float32, device="cuda")
