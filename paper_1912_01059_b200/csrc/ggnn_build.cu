@@ -133,34 +133,37 @@ __global__ void __launch_bounds__(256) leaf_knn_kernel(const __grid_constant__ L
 }
 
 // ------------------------------------------------- leaf kNN on tcgen05 (u8)
-// One CTA (4 warps) per batch of m <= 128 uint8 rows.  The rows are staged in
-// shared memory in the interleaved K-major layout (ggnn_tc.cuh) and serve as
-// both operands of D = X X^T: d/32 tcgen05.mma kind::i8 instructions
-// (M = 128, N = m rounded up to 16, s32 accumulators in 128 TMEM columns),
-// issued by one thread and committed to an mbarrier.  Each thread then owns
-// one row (TMEM lane), reads its dot products with tcgen05.ld and forms exact
-// squared distances n_i + n_j - 2 d_ij (integers, the reference's _sqdist
-// values); every warp selects the k_nn smallest (distance, position) of its
-// 32 rows with the same bitonic top-k as the SIMT kernel -- batch_bruteforce
-// (_core.pyx:107-130) bit for bit.
+// Persistent CTAs of 4 warps, one batch of m <= 128 uint8 rows at a time.
+// The rows are staged in shared memory in the interleaved K-major layout
+// (ggnn_tc.cuh) and serve as both operands of D = X X^T: d/32 tcgen05.mma
+// kind::i8 instructions (M = 128, N = m rounded up to 16, s32 accumulators in
+// 64 or 128 TMEM columns), issued by one thread and committed to an mbarrier.
+// Thread i then owns row i (TMEM lane i): it streams its dot products out of
+// TMEM with tcgen05.ld, forms exact squared distances n_i + n_j - 2 d_ij (the
+// reference's _sqdist values, integers) and keeps the k_nn smallest
+// (distance, position) words in a sorted per-thread list -- ties by
+// position, batch_bruteforce (_core.pyx:107-130) bit for bit.
 constexpr int TC_ROWS = 128;
-constexpr int TC_DSTRIDE = TC_ROWS + 1;
 __device__ int g_tc_timeouts = 0;
 
-inline size_t leaf_tc_smem(int64_t d) {
-  return (size_t)TC_ROWS * d + TC_ROWS * 4 + (size_t)TC_ROWS * TC_DSTRIDE * 4 + 16;
+// staged rows (all 128 MMA rows) + norms + per-thread top-k_nn lists +
+// barrier / TMEM address
+inline size_t leaf_tc_smem(int64_t d, int k_nn) {
+  return (size_t)TC_ROWS * d + TC_ROWS * 4 + (size_t)TC_ROWS * (k_nn + 1) * 8 + 16;
 }
 
+template <uint32_t COLS>
 __global__ void __launch_bounds__(128, 1) leaf_knn_tc_kernel(const __grid_constant__ LeafArgs a, int64_t nbatches) {
   extern __shared__ __align__(16) uint8_t smem_tc[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = (int)a.d;
+  const int lstride = a.k_nn + 1;
   uint8_t* A = smem_tc;
   uint32_t* nrm = reinterpret_cast<uint32_t*>(smem_tc + (size_t)TC_ROWS * K);
-  uint32_t* D = nrm + TC_ROWS;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(D + TC_ROWS * TC_DSTRIDE);
+  uint64_t* lists = reinterpret_cast<uint64_t*>(nrm + TC_ROWS);  // per thread: sorted top-k_nn words
+  uint64_t* mbar = lists + (size_t)TC_ROWS * lstride;
   uint32_t* taddr = reinterpret_cast<uint32_t*>(mbar + 1);
-  if (warp == 0) tc::tmem_alloc<128>(taddr);
+  if (warp == 0) tc::tmem_alloc<COLS>(taddr);
   if (tid == 0) tc::mbar_init(mbar, 1);
   tc::fence_before_sync();
   __syncthreads();
@@ -168,6 +171,7 @@ __global__ void __launch_bounds__(128, 1) leaf_knn_tc_kernel(const __grid_consta
   const uint32_t tmem = *taddr;
   const uint8_t* X = reinterpret_cast<const uint8_t*>(a.X);
   const int nch = K >> 4;
+  uint64_t* mine = lists + (size_t)tid * lstride;
   uint32_t phase = 0;
   // persistent: TMEM and the mbarrier are set up once per CTA
   for (int64_t b = blockIdx.x; b < nbatches; b += gridDim.x, phase ^= 1u) {
@@ -213,6 +217,13 @@ __global__ void __launch_bounds__(128, 1) leaf_knn_tc_kernel(const __grid_consta
     const bool ok = tc::mbar_wait(mbar, phase);
     tc::fence_after_sync();
     if (!ok && lane == 0) atomicAdd(&g_tc_timeouts, 1);
+    // thread tid owns row tid (TMEM lane): stream its products out of TMEM and
+    // keep the k_eff smallest (distance << 32 | position) words -- ties by
+    // position, batch_bruteforce's order -- in its own sorted list
+    const int k_eff = min(a.k_nn, m - 1);
+    if (k_eff < a.k_nn && tid == 0 && a.reduced) atomicAdd(a.reduced, 1);
+    for (int j = 0; j < k_eff; ++j) mine[j] = ~0ull;
+    uint64_t kth = ~0ull;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const uint32_t ni = tid < m ? nrm[tid] : 0u;
     for (int c0 = 0; c0 < n_pad; c0 += 16) {
@@ -221,47 +232,42 @@ __global__ void __launch_bounds__(128, 1) leaf_knn_tc_kernel(const __grid_consta
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int col = c0 + j;
-        if (tid < m && col < m) D[tid * TC_DSTRIDE + col] = ni + nrm[col] - 2u * v[j];
+        if (tid < m && col < m && col != tid && k_eff > 0) {
+          const uint64_t pk = ((uint64_t)(ni + nrm[col] - 2u * v[j]) << 32) | (uint32_t)col;
+          if (pk < kth) {
+            int p = k_eff - 1;
+            while (p > 0 && mine[p - 1] > pk) {
+              mine[p] = mine[p - 1];
+              --p;
+            }
+            mine[p] = pk;
+            kth = mine[k_eff - 1];
+          }
+        }
       }
     }
-    __syncwarp();
-    const int k_eff = min(a.k_nn, m - 1);
-    if (k_eff < a.k_nn && tid == 0 && a.reduced) atomicAdd(a.reduced, 1);
-    for (int i = warp * 32; i < min(m, warp * 32 + 32); ++i) {
-      uint32_t bk = KeyOps<uint32_t>::max_key();
-      int bi = INT_MAX;
-      if (k_eff > 0) {
-        for (int jb = 0; jb < m; jb += 32) {
-          const int j = jb + lane;
-          uint32_t dv = KeyOps<uint32_t>::max_key();
-          int jj = INT_MAX;
-          if (j < m && j != i) {
-            dv = D[i * TC_DSTRIDE + j];
-            jj = j;
-          }
-          topk_merge_chunk(bk, bi, dv, jj, k_eff);
-        }
-      }
-      const int64_t gi = off + i;
-      const double bkd = (double)bk;
-      if (lane < a.k_nn) {
-        const bool v = lane < k_eff;
-        if (a.pos) a.pos[gi * a.k_nn + lane] = v ? bi : -1;
-        if (a.dist) a.dist[gi * a.k_nn + lane] = v ? bkd : KeyOps<double>::max_key();
+    if (tid < m) {
+      const int64_t gi = off + tid;
+      const int32_t node = a.nodes[gi];
+      for (int j = 0; j < a.k_nn; ++j) {
+        const bool v = j < k_eff;
+        const int pos = v ? (int)(uint32_t)mine[j] : -1;
+        const double dd = v ? (double)(uint32_t)(mine[j] >> 32) : KeyOps<double>::max_key();
+        if (a.pos) a.pos[gi * a.k_nn + j] = pos;
+        if (a.dist) a.dist[gi * a.k_nn + j] = dd;
         if (a.adj && v) {
-          const int32_t node = a.nodes[gi];
-          a.adj[(int64_t)node * a.k + lane] = a.nodes[off + bi];
-          a.nnd[(int64_t)node * a.k_nn + lane] = bkd;
+          a.adj[(int64_t)node * a.k + j] = a.nodes[off + pos];
+          a.nnd[(int64_t)node * a.k_nn + j] = dd;
         }
       }
-      if (a.dnn1 && lane == 0) a.dnn1[a.nodes[gi]] = k_eff > 0 ? bkd : KeyOps<double>::max_key();
+      if (a.dnn1) a.dnn1[node] = k_eff > 0 ? (double)(uint32_t)(mine[0] >> 32) : KeyOps<double>::max_key();
     }
     // the next batch overwrites the staged rows and TMEM: everyone must be done
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
   }
-  if (warp == 0) tc::tmem_free<128>(tmem);
+  if (warp == 0) tc::tmem_free<COLS>(tmem);
 }
 
 bool leaf_tc_eligible(const ggnn_vectors* X, int64_t max_batch) {
@@ -549,12 +555,22 @@ static int leaf_knn_impl(const ggnn_vectors* X, const int32_t* d_nodes, const in
   a.reduced = d_reduced;
   cudaStream_t st = as_stream(stream);
   if (leaf_tc_eligible(X, max_batch)) {
-    const size_t smem = leaf_tc_smem(X->d);
-    GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int n_max = std::max(16, (int)((max_batch + 15) & ~int64_t(15)));
+    const size_t smem = leaf_tc_smem(X->d, k_nn);
     DevInfo di = dev_info();
-    const int per_sm = std::max(1, (int)(((size_t)di.smem_optin + 1024) / (smem + 1024)));
-    const int64_t grid = std::min<int64_t>(nbatches, (int64_t)std::max(di.sm_count, 1) * std::min(per_sm, 4));
-    leaf_knn_tc_kernel<<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+    // resident CTAs per SM: shared memory, and TMEM (512 columns / per-CTA columns)
+    const int cols = n_max <= 64 ? 64 : 128;
+    const int per_sm = std::max(1, std::min((int)(((size_t)228 * 1024) / (smem + 1024)), 512 / cols));
+    const int64_t grid = std::min<int64_t>(nbatches, (int64_t)std::max(di.sm_count, 1) * per_sm);
+    if (cols == 64) {
+      GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      leaf_knn_tc_kernel<64><<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+    } else {
+      GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      leaf_knn_tc_kernel<128><<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+    }
     GGNN_LAUNCH_CHECK();
     return GGNN_OK;
   }
