@@ -255,42 +255,67 @@ def _load_ref_hierarchy(root: Path):
     return R, h, meta
 
 
-def _ref_worker(job):
-    """Child process: the reference's own batch_query on a query slice."""
-    root, lo, hi = job
+_REF = None
+
+
+def _ref_init(root):
+    """Worker initializer: load the reference package and the exported graph once."""
+    global _REF
     R, h, meta = _load_ref_hierarchy(Path(root))
-    Q = np.load(Path(root) / "queries.npy", mmap_mode="r")[lo:hi]
+    _REF = (R, h, meta, np.load(Path(root) / "queries.npy", mmap_mode="r"))
+
+
+def _ref_run(job):
+    """The reference's own batch_query on a query slice (timed inside the worker)."""
+    lo, hi = job
+    R, h, meta, Q = _REF
+    q = np.ascontiguousarray(Q[lo:hi])
     t0 = time.perf_counter()
-    res = R.batch_query(h, np.ascontiguousarray(Q), R.QueryConfig(k_out=10, tau=meta["tau"]), threads=1)
+    res = R.batch_query(h, q, R.QueryConfig(k_out=10, tau=meta["tau"]), threads=1)
     dt = time.perf_counter() - t0
     ids = np.stack([np.pad(r.ids, (0, 10 - len(r.ids)), constant_values=-1) for r in res])
     return dt, ids
 
 
-def cpu_reference_qps(root: Path, nq_total: int, target_seconds: float, max_procs=None):
+class RefPool:
     """Process-parallel reference batch_query (threads do not scale under the
-    GIL): one process per host core on a bounded query sample."""
-    import multiprocessing as mp
+    GIL): one process per host core, each holding the exported
+    GPU-built graph, answering bounded query samples of the workload."""
 
-    cores = max_procs or os.cpu_count() or 1
-    ctx = mp.get_context("spawn")
-    probe = min(20, nq_total)
-    with ctx.Pool(1) as pool:
-        dt, _ = pool.map(_ref_worker, [(str(root), 0, probe)])[0]
-    per_q = dt / probe
-    per_proc = max(1, int(target_seconds / max(per_q, 1e-6)))
-    per_proc = min(per_proc, max(1, nq_total // cores))
-    jobs = [(str(root), i * per_proc, (i + 1) * per_proc) for i in range(cores) if (i + 1) * per_proc <= nq_total]
-    with ctx.Pool(len(jobs)) as pool:
-        out = pool.map(_ref_worker, jobs)
-    inner = max(o[0] for o in out)
-    nq = sum(j[2] - j[1] for j in jobs)
-    ids = np.concatenate([o[1] for o in out])
-    tau = json.loads((root / "meta.json").read_text())["tau"]
-    return {"value": nq / inner, "unit": UNIT, "cores": len(jobs), "kind": "reference",
-            "sample": f"{nq} queries ({len(jobs)} processes x {per_proc}) of the same workload on the GPU-built "
-                      f"graph, reference graphann.batch_query (compiled _core), tau={tau}",
-            "ids": ids, "n": nq}
+    def __init__(self, root: Path, nq_total: int, procs=None):
+        import multiprocessing as mp
+
+        self.root, self.nq = root, nq_total
+        self.procs = procs or os.cpu_count() or 1
+        self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_ref_init, initargs=(str(root),))
+        probe = min(20, nq_total)
+        dt, _ = self.pool.map(_ref_run, [(0, probe)])[0]
+        self.per_q = dt / probe
+        self.tau = json.loads((root / "meta.json").read_text())["tau"]
+
+    def sample(self, target_seconds: float) -> dict:
+        per_proc = max(1, int(target_seconds / max(self.per_q, 1e-6)))
+        per_proc = min(per_proc, max(1, self.nq // self.procs))
+        jobs = [(i * per_proc, (i + 1) * per_proc) for i in range(self.procs) if (i + 1) * per_proc <= self.nq]
+        out = self.pool.map(_ref_run, jobs, chunksize=1)
+        inner = max(o[0] for o in out)
+        nq = sum(hi - lo for lo, hi in jobs)
+        return {"value": nq / inner, "unit": UNIT, "cores": len(jobs), "kind": "reference",
+                "sample": f"{nq} queries ({len(jobs)} processes x {per_proc}) of the same workload on the GPU-built "
+                          f"graph, reference graphann.batch_query (compiled _core), tau={self.tau}",
+                "ids": np.concatenate([o[1] for o in out]), "n": nq}
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+
+def cpu_reference_qps(root: Path, nq_total: int, target_seconds: float, max_procs=None):
+    pool = RefPool(root, nq_total, max_procs)
+    try:
+        return pool.sample(target_seconds)
+    finally:
+        pool.close()
 
 
 # ------------------------------------------------------------------ main
@@ -618,18 +643,23 @@ def run_reference(args, dist, ga):
     import shutil
 
     root = export_graph(h, base, Q, tau)
-    per_step = max(5.0, min(args.cpu_seconds, 240.0 / max(1, args.steps + args.warmup)))
+    # one worker pool for the whole run; each step is a bounded sample
+    per_step = max(2.0, min(args.cpu_seconds, 180.0 / max(1, args.steps + args.warmup)))
     vals = []
     info = None
+    pool = None
     try:
+        pool = RefPool(root, Q.shape[0])
         for i in range(args.warmup + args.steps):
-            r = cpu_reference_qps(root, Q.shape[0], per_step)
+            r = pool.sample(per_step)
             r.pop("ids")
             r.pop("n")
             if i >= args.warmup:
                 vals.append(r["value"])
                 info = r
     finally:
+        if pool is not None:
+            pool.close()
         shutil.rmtree(root, ignore_errors=True)
     value = float(np.mean(vals))
     line = {
