@@ -17,10 +17,9 @@ from .config import QueryConfig
 from .device import DeviceVectors, device_hierarchy
 
 TERMINATED_BY = {0: "stopping-rule", 1: "queue-empty", 2: "iteration-cap"}
-_TERM_CODE = {v: k for k, v in TERMINATED_BY.items()}
 
-# queries per launch when exact distinct_touched is requested (its per-query
-# diagnostic set lives in device workspace)
+# queries per rerun launch when a compact distinct-set overflowed (their exact
+# per-query sets live in device workspace, up to 256 KB each)
 _DISTINCT_CHUNK = 512
 
 
@@ -359,8 +358,9 @@ def descent_arrays(h, queries, cfg: QueryConfig, start: int, stop: int, seg_lo=N
 
 
 def exact_knn_rows(dataset, rows: np.ndarray, k: int):
-    """Exact top-k (k <= 32) of dataset rows `rows` against the whole dataset,
-    ties by ascending id, in one launch of ggnn_exhaustive_topk."""
+    """Exact top-k of dataset rows `rows` against the whole dataset, ties by
+    ascending id, in one ggnn_exhaustive_topk launch (k <= 32; up to 128 on
+    the tensor-core path for uint8 tables)."""
     dv = DeviceVectors.of(dataset)
     rows = np.ascontiguousarray(rows, dtype=np.int32)
     t = N.torch()
@@ -374,8 +374,9 @@ def exact_knn_rows(dataset, rows: np.ndarray, k: int):
 
 
 def exact_knn(dataset, queries: np.ndarray, k: int):
-    """Exact top-k (k <= 32) of external queries against the whole dataset,
-    ties by ascending id (ground truth for recall), one launch."""
+    """Exact top-k of external queries against the whole dataset, ties by
+    ascending id (ground truth for recall), one launch (k limits as
+    exact_knn_rows)."""
     dv = DeviceVectors.of(dataset)
     dq, qs = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
     t = N.torch()
