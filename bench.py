@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--tau", type=float, default=None, help="skip the sweep and use this tau")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: NCCL all-gather after the search, or the fused peer-memory exchange")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -541,7 +543,17 @@ def run_sharded(args, dist, ga, torch):
     stream = torch.cuda.current_stream()
     qev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
 
+    x = grp.p2p(m, 10) if args.exchange == "p2p" else None
+
     def step(i=None):
+        if x is not None:  # fused: push search + signal, then wait + merge
+            if i is not None:
+                qev[2 * i].record(stream)
+            x.search_push(h, Q, qcfg)
+            if i is not None:
+                qev[2 * i + 1].record(stream)
+            x.merge_into(out_ids, out_d, out_c)
+            return
         if i is not None:
             qev[2 * i].record(stream)
         N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
@@ -571,11 +583,16 @@ def run_sharded(args, dist, ga, torch):
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
+    if x is not None:
+        x.check()
     t_max = dist.max(evs[0].elapsed_time(evs[-1]) / 1e3)
     value = G * m * args.steps / t_max
     kern = float(np.mean([qev[2 * i].elapsed_time(qev[2 * i + 1]) for i in range(args.steps)])) / 1e3
     coff = block_layout(m, 10)[2]
-    own = send[coff:coff + m * 20].view(torch.int32).view(m, 5).cpu().numpy()  # this rank's V, T counters
+    if x is not None:
+        own = x.local_cnt.cpu().numpy()
+    else:
+        own = send[coff:coff + m * 20].view(torch.int32).view(m, 5).cpu().numpy()  # this rank's V, T counters
     e = 1 if dv.exact_integers else 4
     bpl = _bytes_per_launch(own, args.d, e, dh.layers[0].k, 10)
     peak, peak_src = _peak()
@@ -583,12 +600,12 @@ def run_sharded(args, dist, ga, torch):
 
     Q_host = np.ascontiguousarray(Q, dtype=np.float32)
     for _ in range(max(1, args.warmup)):
-        grp.query_arrays(Q_host, qcfg)
+        grp.query_arrays(Q_host, qcfg, exchange=args.exchange)
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        out = grp.query_arrays(Q_host, qcfg)
+        out = grp.query_arrays(Q_host, qcfg, exchange=args.exchange)
     torch.cuda.synchronize()
     e2e_t = dist.max(time.perf_counter() - t0)
     line = {
@@ -603,7 +620,10 @@ def run_sharded(args, dist, ga, torch):
                    "tau": tau, "recall_merged": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
                    "mean_visited_per_shard": chosen["V"], "mean_steps_per_shard": chosen["T"], "tau_sweep": sweep,
                    "build_seconds_max_over_ranks": build_s,
-                   "parallelism": f"sharded x{G}: NCCL all_gather_into_tensor of {bb} B/rank + ggnn_shard_merge",
+                   "parallelism": (f"sharded x{G}: NCCL all_gather_into_tensor of {bb} B/rank + ggnn_shard_merge"
+                                   if x is None else f"sharded x{G}: fused exchange (query kernel stores each "
+                                   f"finished row into every peer's receive block over CUDA IPC) + "
+                                   f"ggnn_shard_merge_wait"),
                    "l2": "inputs larger than L2 (u8 shard 128 MB + adjacency 96 MB per GPU)"},
         "build_seconds": build_s,
         "e2e": {"value": G * m * args.steps / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(m * args.d * e),
@@ -621,6 +641,7 @@ def run_sharded(args, dist, ga, torch):
         print(js, flush=True)
         if args.out:
             Path(args.out).write_text(js + "\n")
+    grp.close()
     dist.close()
 
 

@@ -45,6 +45,11 @@ class SearchParams(ctypes.Structure):
                 ("max_iterations", I64)]
 
 
+class Push(ctypes.Structure):  # ggnn_push (include/ggnn_p2p.h)
+    _fields_ = [("d_peers", P * 8), ("nranks", I32), ("rank", I32), ("parity", I32), ("pad_", I32),
+                ("d_gid_of_local", P), ("gid_size", I64)]
+
+
 class NativeError(RuntimeError):
     pass
 
@@ -83,10 +88,19 @@ _SIGS = {
     "ggnn_shard_block_counters_offset": [I64, I32],
     "ggnn_shard_globalize": [P, I64, P, I64, P],
     "ggnn_shard_merge": [P, I32, I64, I32, I32, P, P, P, P],
+    "ggnn_p2p_bytes": [I32, I64, I32],
+    "ggnn_p2p_alloc": [ctypes.c_size_t, P, P],
+    "ggnn_p2p_open": [P, P],
+    "ggnn_p2p_close": [P],
+    "ggnn_p2p_free": [P],
+    "ggnn_query_batch_push": [P, P, P, I64, P, P, F64, P, P, P, P, P],
+    "ggnn_p2p_signal": [P, I64, I32, ctypes.c_uint32, P],
+    "ggnn_shard_merge_wait": [P, I32, ctypes.c_uint32, I32, I64, I32, I32, P, P, P, P, P],
 }
 _RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t,
              "ggnn_layer_stats_scratch_bytes": ctypes.c_size_t, "ggnn_shard_block_bytes": ctypes.c_size_t,
-             "ggnn_shard_block_dists_offset": ctypes.c_size_t, "ggnn_shard_block_counters_offset": ctypes.c_size_t}
+             "ggnn_shard_block_dists_offset": ctypes.c_size_t, "ggnn_shard_block_counters_offset": ctypes.c_size_t,
+             "ggnn_p2p_bytes": ctypes.c_size_t}
 # entry points added by later translation units register themselves here
 EXTRA_SIGS: dict = {}
 

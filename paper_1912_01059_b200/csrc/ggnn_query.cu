@@ -12,7 +12,9 @@
 
 #include "ggnn_build.h"
 #include "ggnn_capi_util.cuh"
+#include "ggnn_p2p.h"
 #include "ggnn_search.cuh"
+#include "ggnn_shard.h"
 
 namespace ggnn {
 
@@ -114,6 +116,13 @@ struct SearchArgs {
   int seg_div;
   int seg_size;
   int* work;  // persistent-warp item counter (nullptr: one item per warp)
+  // fused sharded exchange (ggnn_query_batch_push): block `push_rank` of
+  // parity half `push_parity` of every receive allocation
+  uint8_t* push_peers[GGNN_P2P_MAX_RANKS];
+  int push_n, push_rank;
+  size_t push_half, push_bb, push_doff, push_coff;
+  const int32_t* push_gid;
+  int64_t push_gid_size;
 };
 
 // Persistent warps: with a work counter (zeroed before the launch) every warp
@@ -210,8 +219,31 @@ __device__ void write_hits(const WarpSearch<TX, TQ, LP>& s, const SearchArgs& a,
   }
 }
 
+// Fused exchange: this query's row, ids globalized, into block push_rank of
+// every receive allocation (NVLink stores to peer GPUs; the own one is local).
+__device__ __forceinline__ void push_row(const SearchArgs& a, int64_t qi) {
+  const int lane = lane_id();
+  const int k = a.c.k_out;
+  const int64_t base = (int64_t)a.push_rank * (int64_t)a.push_bb;
+  if (lane < k) {
+    const int32_t id = a.ids[qi * k + lane];
+    const double dv = a.dists[qi * k + lane];
+    const int32_t gid = (id >= 0 && id < a.push_gid_size) ? __ldg(a.push_gid + id) : -1;
+    for (int g = 0; g < a.push_n; ++g) {
+      uint8_t* blk = a.push_peers[g] + base;
+      reinterpret_cast<int32_t*>(blk)[qi * k + lane] = gid;
+      reinterpret_cast<double*>(blk + a.push_doff)[qi * k + lane] = dv;
+    }
+  }
+  if (lane < 5 && a.counters) {
+    const int32_t c = a.counters[qi * 5 + lane];
+    for (int g = 0; g < a.push_n; ++g)
+      reinterpret_cast<int32_t*>(a.push_peers[g] + base + a.push_coff)[qi * 5 + lane] = c;
+  }
+}
+
 // ------------------------------------------------------------------ query()
-template <typename TX, typename TQ, int LP>
+template <typename TX, typename TQ, int LP, bool PUSH = false>
 __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* smem_w, int* vring_lane, int64_t qi) {
   using Key = typename VecTraits<TX, TQ>::Key;
   const int lane = lane_id();
@@ -234,19 +266,23 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
   s.run();
   // query() adds the top scan to the effort counters (search.py:134-136)
   write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
+  if constexpr (PUSH) {
+    __syncwarp();
+    push_row(a, qi);
+  }
 }
 
-template <typename TX, typename TQ, int LP>
+template <typename TX, typename TQ, int LP, bool PUSH = false>
 __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
   if constexpr (GGNN_PERSISTENT != 0) {
     for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
-      query_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+      query_kernel_one<TX, TQ, LP, PUSH>(a, smem_w, vring_lane, qi);
   } else {
     const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (qi < a.m) query_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
+    if (qi < a.m) query_kernel_one<TX, TQ, LP, PUSH>(a, smem_w, vring_lane, qi);
   }
 }
 
@@ -834,6 +870,55 @@ int ggnn_query_batch(const ggnn_vectors* X, const ggnn_layer* bottom, const int3
     case 0: return GGNN_LAUNCH_LP(query_kernel, float, float, a, a.m, a.region, st);
     case 1: return GGNN_LAUNCH_LP(query_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
     default: return launch_warps(query_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
+  }
+}
+
+int ggnn_query_batch_push(const ggnn_vectors* X, const ggnn_layer* bottom, const int32_t* d_top_rows, int64_t ntop,
+                          const ggnn_queries* Q, const ggnn_search_params* p, double d_nn1_max, int32_t* d_ids,
+                          double* d_dists, int32_t* d_counters, const ggnn_push* push, void* stream) {
+  SearchArgs a;
+  int rc = fill_common(a, X, Q, p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(!(p->flags & GGNN_FLAG_DISTINCT), "the push search does not track distinct_touched");
+  GGNN_CHECK_ARG(bottom && bottom->d_adj && bottom->k >= 1 && bottom->k <= MAX_K, "invalid bottom layer");
+  GGNN_CHECK_ARG(ntop >= 1, "the top layer is empty");
+  GGNN_CHECK_ARG(d_ids && d_dists && d_counters, "null outputs");
+  GGNN_CHECK_ARG(push && push->nranks >= 1 && push->nranks <= GGNN_P2P_MAX_RANKS && push->rank >= 0 &&
+                     push->rank < push->nranks && (push->parity == 0 || push->parity == 1) && push->d_gid_of_local,
+                 "invalid push descriptor");
+  a.layer = to_dev(*bottom);
+  a.top_rows = d_top_rows;
+  a.ntop = ntop;
+  a.dmax = d_nn1_max;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  a.counters = d_counters;
+  a.ever_cap = INT_MAX;
+  const size_t bb = ggnn_shard_block_bytes(a.m, p->k_out);
+  const size_t half = (size_t)push->nranks * bb + (((size_t)push->nranks * 4 + 255) & ~size_t(255));
+  for (int g = 0; g < push->nranks; ++g) {
+    GGNN_CHECK_ARG(push->d_peers[g] != nullptr, "push: receive allocation %d missing", g);
+    a.push_peers[g] = static_cast<uint8_t*>(push->d_peers[g]) + (size_t)push->parity * half;
+  }
+  a.push_n = push->nranks;
+  a.push_rank = push->rank;
+  a.push_half = half;
+  a.push_bb = bb;
+  a.push_doff = ggnn_shard_block_dists_offset(a.m, p->k_out);
+  a.push_coff = ggnn_shard_block_counters_offset(a.m, p->k_out);
+  a.push_gid = push->d_gid_of_local;
+  a.push_gid_size = push->gid_size;
+  cudaStream_t st = as_stream(stream);
+  switch (combo(X, Q)) {
+    case 0:
+      if (a.lpr == 32) return launch_warps(query_kernel<float, float, 32, true>, a, a.m, a.region, st);
+      if (a.lpr == 8) return launch_warps(query_kernel<float, float, 8, true>, a, a.m, a.region, st);
+      return launch_warps(query_kernel<float, float, 0, true>, a, a.m, a.region, st);
+    case 1:
+      if (a.lpr == 32) return launch_warps(query_kernel<uint8_t, uint8_t, 32, true>, a, a.m, a.region, st);
+      if (a.lpr == 8) return launch_warps(query_kernel<uint8_t, uint8_t, 8, true>, a, a.m, a.region, st);
+      return launch_warps(query_kernel<uint8_t, uint8_t, 0, true>, a, a.m, a.region, st);
+    default: return launch_warps(query_kernel<uint8_t, float, 0, true>, a, a.m, a.region, st);
   }
 }
 

@@ -10,6 +10,7 @@
 // shards are disjoint), which gives terminated_by (shard.py:108).
 #include <climits>
 #include "ggnn_capi_util.cuh"
+#include "ggnn_p2p.h"
 #include "ggnn_search.cuh"
 #include "ggnn_shard.h"
 
@@ -42,9 +43,36 @@ struct MergeShardArgs {
   int32_t* out_ids;
   double* out_dists;
   int32_t* out_cnt;
+  // fused exchange: wait until every flags[g] == epoch (nullptr: no wait)
+  const uint32_t* flags;
+  uint32_t epoch;
+  int32_t* error;
 };
 
+// Bounded acquire-spin of one thread on G peer-written flags (~10 s at
+// 2 GHz, then *error = 1 and the merge proceeds on whatever arrived).
+__device__ void wait_flags(const uint32_t* flags, int G, uint32_t epoch, int32_t* error) {
+  const long long t0 = clock64();
+  for (int g = 0; g < G; ++g) {
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + g) : "memory");
+      if (v == epoch) break;
+      if (clock64() - t0 > 20000000000ll) {
+        if (error) atomicExch(error, 1);
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+  __threadfence();
+}
+
 __global__ void __launch_bounds__(256) shard_merge_kernel(const __grid_constant__ MergeShardArgs a) {
+  if (a.flags) {
+    if (threadIdx.x == 0) wait_flags(a.flags, a.G, a.epoch, a.error);
+    __syncthreads();
+  }
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= a.m) return;
   const int lane = lane_id();
@@ -112,10 +140,74 @@ __global__ void __launch_bounds__(256) shard_merge_kernel(const __grid_constant_
   }
 }
 
+struct SignalArgs {
+  uint32_t* flags[GGNN_P2P_MAX_RANKS];  // flag `rank` of every receive allocation (parity half)
+  int G;
+  uint32_t epoch;
+};
+
+__global__ void p2p_signal_kernel(const __grid_constant__ SignalArgs a) {
+  const int g = threadIdx.x;
+  if (g >= a.G) return;
+  __threadfence_system();  // this rank's pushed rows are visible system-wide first
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.flags[g]), "r"(a.epoch) : "memory");
+}
+
+inline size_t p2p_half(int G, int64_t m, int k) {
+  return (size_t)G * block_bytes(m, k) + (((size_t)G * 4 + 255) & ~size_t(255));
+}
+
 }  // namespace
 }  // namespace ggnn
 
 using namespace ggnn;
+
+extern "C" size_t ggnn_p2p_bytes(int32_t G, int64_t m, int32_t k) { return 2 * p2p_half(G, m, k); }
+
+extern "C" int ggnn_p2p_alloc(size_t bytes, void** d_ptr, void* ipc_handle_out) {
+  GGNN_CHECK_ARG(d_ptr && ipc_handle_out && bytes > 0, "ggnn_p2p_alloc: invalid arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == GGNN_IPC_HANDLE_BYTES, "IPC handle size");
+  GGNN_CUDA_TRY(cudaMalloc(d_ptr, bytes));
+  GGNN_CUDA_TRY(cudaMemset(*d_ptr, 0, bytes));
+  cudaIpcMemHandle_t h;
+  GGNN_CUDA_TRY(cudaIpcGetMemHandle(&h, *d_ptr));
+  memcpy(ipc_handle_out, &h, sizeof(h));
+  return GGNN_OK;
+}
+
+extern "C" int ggnn_p2p_open(const void* ipc_handle, void** d_peer_ptr) {
+  GGNN_CHECK_ARG(ipc_handle && d_peer_ptr, "ggnn_p2p_open: invalid arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  GGNN_CUDA_TRY(cudaIpcOpenMemHandle(d_peer_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return GGNN_OK;
+}
+
+extern "C" int ggnn_p2p_close(void* d_peer_ptr) {
+  GGNN_CUDA_TRY(cudaIpcCloseMemHandle(d_peer_ptr));
+  return GGNN_OK;
+}
+
+extern "C" int ggnn_p2p_free(void* d_ptr) {
+  GGNN_CUDA_TRY(cudaFree(d_ptr));
+  return GGNN_OK;
+}
+
+extern "C" int ggnn_p2p_signal(const ggnn_push* push, int64_t m, int32_t k, uint32_t epoch, void* stream) {
+  GGNN_CHECK_ARG(push && push->nranks >= 1 && push->nranks <= GGNN_P2P_MAX_RANKS && push->rank >= 0 &&
+                     push->rank < push->nranks && (push->parity == 0 || push->parity == 1),
+                 "invalid push descriptor");
+  const size_t half = p2p_half(push->nranks, m, k);
+  SignalArgs a;
+  a.G = push->nranks;
+  a.epoch = epoch;
+  for (int g = 0; g < push->nranks; ++g)
+    a.flags[g] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(push->d_peers[g]) + (size_t)push->parity * half +
+                                             (size_t)push->nranks * block_bytes(m, k)) + push->rank;
+  p2p_signal_kernel<<<1, 32, 0, as_stream(stream)>>>(a);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
 
 extern "C" size_t ggnn_shard_block_bytes(int64_t m, int32_t k_in) { return block_bytes(m, k_in); }
 extern "C" size_t ggnn_shard_block_dists_offset(int64_t m, int32_t k_in) { return block_dists_off(m, k_in); }
@@ -134,8 +226,30 @@ extern "C" int ggnn_shard_globalize(int32_t* d_ids, int64_t count, const int32_t
   return GGNN_OK;
 }
 
+static int shard_merge_impl(const void* d_blocks, int32_t G, int64_t m, int32_t k_in, int32_t k_out,
+                            int32_t* d_out_ids, double* d_out_dists, int32_t* d_out_counters, const uint32_t* flags,
+                            uint32_t epoch, int32_t* error, void* stream);
+
 extern "C" int ggnn_shard_merge(const void* d_blocks, int32_t G, int64_t m, int32_t k_in, int32_t k_out,
                                 int32_t* d_out_ids, double* d_out_dists, int32_t* d_out_counters, void* stream) {
+  return shard_merge_impl(d_blocks, G, m, k_in, k_out, d_out_ids, d_out_dists, d_out_counters, nullptr, 0u, nullptr,
+                          stream);
+}
+
+extern "C" int ggnn_shard_merge_wait(const void* d_recv, int32_t parity, uint32_t epoch, int32_t G, int64_t m,
+                                     int32_t k, int32_t k_out, int32_t* d_out_ids, double* d_out_dists,
+                                     int32_t* d_out_counters, int32_t* d_error, void* stream) {
+  GGNN_CHECK_ARG(d_recv && (parity == 0 || parity == 1) && G >= 1 && G <= GGNN_P2P_MAX_RANKS,
+                 "ggnn_shard_merge_wait: invalid arguments");
+  const uint8_t* half = static_cast<const uint8_t*>(d_recv) + (size_t)parity * p2p_half(G, m, k);
+  const uint32_t* flags = reinterpret_cast<const uint32_t*>(half + (size_t)G * block_bytes(m, k));
+  return shard_merge_impl(half, G, m, k, k_out, d_out_ids, d_out_dists, d_out_counters, flags, epoch, d_error,
+                          stream);
+}
+
+static int shard_merge_impl(const void* d_blocks, int32_t G, int64_t m, int32_t k_in, int32_t k_out,
+                            int32_t* d_out_ids, double* d_out_dists, int32_t* d_out_counters, const uint32_t* flags,
+                            uint32_t epoch, int32_t* error, void* stream) {
   GGNN_CHECK_ARG(G >= 1 && m >= 0 && k_in >= 1, "ggnn_shard_merge: bad shape G=%d m=%lld k_in=%d", G, (long long)m,
                  k_in);
   GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32, "ggnn_shard_merge: k_out must be in [1, 32], got %d", k_out);
@@ -153,6 +267,9 @@ extern "C" int ggnn_shard_merge(const void* d_blocks, int32_t G, int64_t m, int3
   a.out_ids = d_out_ids;
   a.out_dists = d_out_dists;
   a.out_cnt = d_out_counters;
+  a.flags = flags;
+  a.epoch = epoch;
+  a.error = error;
   const int wpb = 8;
   const int64_t blocks = (m + wpb - 1) / wpb;
   shard_merge_kernel<<<(unsigned)blocks, wpb * 32, 0, as_stream(stream)>>>(a);

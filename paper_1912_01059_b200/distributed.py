@@ -130,20 +130,141 @@ class ShardGroup:
             return ids, dists
         return np.asarray(ids.cpu()), np.asarray(dists.cpu())
 
-    def query_arrays(self, queries: np.ndarray, cfg: QueryConfig | None = None, out: str = "numpy"):
+    def query_arrays(self, queries: np.ndarray, cfg: QueryConfig | None = None, out: str = "numpy",
+                     exchange: str = "nccl"):
         """Sharded query of a replicated batch; every rank returns the merged
-        global result (shard.py:113-128 for the whole batch)."""
+        global result (shard.py:113-128 for the whole batch).  exchange="p2p"
+        fuses the exchange into the search (P2PExchange); same results."""
         cfg = cfg or QueryConfig()
         Q = np.ascontiguousarray(queries, dtype=np.float32)
         if Q.ndim == 1:
             Q = Q[None, :]
         m = Q.shape[0]
-        bb = self.block_bytes(m, cfg.k_out)
-        send = self.new_buffer(bb)
-        recv = self.new_buffer(self.world * bb)
-        self.search_block(Q, cfg, send)
-        self.exchange(send, recv)
-        ids, dists, cnt = self.merge(recv, m, cfg)
+        if exchange == "p2p":
+            ids, dists, cnt = self.p2p(m, cfg.k_out).query(Q, cfg)
+        elif exchange == "nccl":
+            bb = self.block_bytes(m, cfg.k_out)
+            send = self.new_buffer(bb)
+            recv = self.new_buffer(self.world * bb)
+            self.search_block(Q, cfg, send)
+            self.exchange(send, recv)
+            ids, dists, cnt = self.merge(recv, m, cfg)
+        else:
+            raise ValueError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
         if out == "device":
             return ids, dists, cnt
         return BatchResult(np.asarray(ids.cpu()), np.asarray(dists.cpu()), np.asarray(cnt.cpu()))
+
+    def p2p(self, m: int, k: int) -> "P2PExchange":
+        """The (collectively created) fused-exchange state for batches of m
+        queries and k results; cached per (m, k).  Every rank must call it
+        with the same arguments in the same order."""
+        cache = self.__dict__.setdefault("_p2p", {})
+        if (m, k) not in cache:
+            cache[(m, k)] = P2PExchange(self, m, k)
+        return cache[(m, k)]
+
+    def close(self) -> None:
+        """Release the fused-exchange mappings (collective)."""
+        for x in self.__dict__.pop("_p2p", {}).values():
+            x.close()
+
+
+class P2PExchange:
+    """Search and exchange fused over peer memory (include/ggnn_p2p.h).
+
+    Every rank owns one receive allocation of two parity halves, each G shard
+    blocks + G flags, and maps every peer's allocation through CUDA IPC (over
+    NVLink / NVSwitch on a multi-GPU node; two ranks on one GPU work too).
+    One step on the rank's stream:
+      ggnn_query_batch_push   -- each warp stores its finished query's
+                                 globalized row into block `rank` of all G
+                                 allocations (transfer overlaps the search)
+      ggnn_p2p_signal         -- system fence, epoch -> flag `rank` everywhere
+      ggnn_shard_merge_wait   -- spin (bounded) on the G local flags, merge
+    Epoch e uses parity e & 1: a rank can only reach epoch e after every
+    peer signalled e - 1, which on that peer's stream follows its merge of
+    e - 2, so a half is never overwritten while it is being merged."""
+
+    def __init__(self, grp: ShardGroup, m: int, k: int):
+        t = N.torch()
+        self.grp, self.m, self.k, self.G, self.rank = grp, m, k, grp.world, grp.rank
+        if self.G > 8:
+            raise ValueError("the fused exchange supports at most 8 ranks")
+        nbytes = N.load().ggnn_p2p_bytes(self.G, m, k)
+        self.own = N.P()
+        handle = (N.ctypes.c_uint8 * 64)()
+        N.call("ggnn_p2p_alloc", N.ctypes.c_size_t(nbytes), N.ctypes.byref(self.own), handle)
+        handles = [None] * self.G
+        grp.dist.all_gather_object(handles, bytes(handle), group=grp.group)
+        self.peers = []
+        for g, hb in enumerate(handles):
+            if g == self.rank:
+                self.peers.append(self.own)
+                continue
+            p = N.P()
+            buf = (N.ctypes.c_uint8 * 64).from_buffer_copy(hb)
+            N.call("ggnn_p2p_open", buf, N.ctypes.byref(p))
+            self.peers.append(p)
+        grp.dist.barrier(group=grp.group)
+        self.epoch = 0
+        self.push = N.Push()
+        for g, p in enumerate(self.peers):
+            self.push.d_peers[g] = p
+        self.push.nranks, self.push.rank = self.G, self.rank
+        gid = grp.gid_dev()
+        self.push.d_gid_of_local, self.push.gid_size = N.ptr(gid), int(grp.gid_host.shape[0])
+        self.error = t.zeros((1,), dtype=t.int32, device=N.device())
+        # the shard-local results (unused by the merge) land here
+        self.local_ids = N.empty((m, k), t.int32)
+        self.local_dists = N.empty((m, k), t.float64)
+        self.local_cnt = N.empty((m, 5), t.int32)
+
+    def search_push(self, h, Q: np.ndarray, cfg: QueryConfig) -> None:
+        """Launch the push search + signal of the next epoch (no merge)."""
+        from .device import device_hierarchy
+        from .search import _flags, _params
+
+        if Q.shape[0] != self.m or cfg.k_out != self.k:
+            raise ValueError("batch shape does not match this exchange")
+        self.epoch += 1
+        self.push.parity = self.epoch & 1
+        dh = device_hierarchy(h)
+        dv = dh.vectors
+        dq, qs = dv.queries(Q)
+        params = _params(cfg, _flags(dv, False))
+        N.call("ggnn_query_batch_push", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
+               N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max,
+               N.ptr(self.local_ids), N.ptr(self.local_dists), N.ptr(self.local_cnt), N.ctypes.byref(self.push),
+               N.stream_ptr())
+        N.call("ggnn_p2p_signal", N.ctypes.byref(self.push), self.m, self.k, N.ctypes.c_uint32(self.epoch),
+               N.stream_ptr())
+        self._dq = dq  # keep the device queries alive until the stream passes them
+
+    def merge_into(self, ids, dists, cnt) -> None:
+        N.call("ggnn_shard_merge_wait", self.own, self.epoch & 1, N.ctypes.c_uint32(self.epoch), self.G, self.m,
+               self.k, self.k, N.ptr(ids), N.ptr(dists), N.ptr(cnt), N.ptr(self.error), N.stream_ptr())
+
+    def query(self, Q: np.ndarray, cfg: QueryConfig):
+        t = N.torch()
+        self.search_push(self.grp.h, Q, cfg)
+        ids = N.empty((self.m, self.k), t.int32)
+        dists = N.empty((self.m, self.k), t.float64)
+        cnt = N.empty((self.m, 5), t.int32)
+        self.merge_into(ids, dists, cnt)
+        self.check()
+        return ids, dists, cnt
+
+    def check(self) -> None:
+        if int(self.error.item()):
+            raise N.NativeError("fused exchange: a peer's rows did not arrive within the wait bound")
+
+    def close(self) -> None:
+        N.torch().cuda.synchronize()
+        self.grp.dist.barrier(group=self.grp.group)  # nobody writes into our allocation any more
+        for g, p in enumerate(self.peers):
+            if g != self.rank:
+                N.call("ggnn_p2p_close", p)
+        self.grp.dist.barrier(group=self.grp.group)
+        N.call("ggnn_p2p_free", self.own)
+        self.peers = []

@@ -142,6 +142,64 @@ def test_brute_force_oracle_and_knn_graph():
         np.testing.assert_array_equal(kg[i], [v for v in ids if v != i][:3])
 
 
+def test_fused_exchange_kernels_one_process():
+    """The push search + signal + merge-wait kernels with G = 3 "ranks" in
+    one process (own allocations, no IPC): every rank's merged result equals
+    the unfused block search + ggnn_shard_merge, over 4 epochs (both
+    parities, each reused)."""
+    import ctypes
+
+    import torch
+
+    from paper_1912_01059_b200.search import _flags, _params
+    from paper_1912_01059_b200.device import device_hierarchy
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, Q = make_latent16(n=3000, d=32, m=130, seed=5)
+    ds = ga.Dataset(base)
+    si, _ = ga.build_sharded(ds, 1000, ga.BuildConfig(seed=7))
+    G, m = len(si.shards), Q.shape[0]
+    allocs = []
+    for _ in range(G):
+        p, hd = ctypes.c_void_p(), (ctypes.c_uint8 * 64)()
+        N.call("ggnn_p2p_alloc", ctypes.c_size_t(N.load().ggnn_p2p_bytes(G, m, 10)), ctypes.byref(p), hd)
+        allocs.append(p)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    gids = [si.gid_of_local(g) for g in range(G)]
+    try:
+        for epoch, tau in zip(range(1, 5), (0.6, 0.3, 0.6, 0.5)):
+            cfg = ga.QueryConfig(k_out=10, tau=tau)
+            ref = ga.query_sharded_arrays(si, Q, cfg)
+            keep = []
+            for g, (_, h) in enumerate(si.shards):
+                push = N.Push()
+                for j in range(G):
+                    push.d_peers[j] = allocs[j]
+                push.nranks, push.rank, push.parity = G, g, epoch & 1
+                push.d_gid_of_local, push.gid_size = N.ptr(gids[g]), int(gids[g].numel())
+                dh = device_hierarchy(h)
+                dq, qs = dh.vectors.queries(Q)
+                loc = [N.empty((m, 10), torch.int32), N.empty((m, 10), torch.float64), N.empty((m, 5), torch.int32)]
+                N.call("ggnn_query_batch_push", ctypes.byref(dh.vectors.struct), ctypes.byref(dh.layers[0].struct),
+                       N.ptr(dh.top_rows), dh.ntop, ctypes.byref(qs),
+                       ctypes.byref(_params(cfg, _flags(dh.vectors, False))), dh.d_nn1_max, *map(N.ptr, loc),
+                       ctypes.byref(push), N.stream_ptr())
+                N.call("ggnn_p2p_signal", ctypes.byref(push), m, 10, ctypes.c_uint32(epoch), N.stream_ptr())
+                keep += [dq, loc]
+            for g in range(G):
+                out = [N.empty((m, 10), torch.int32), N.empty((m, 10), torch.float64), N.empty((m, 5), torch.int32)]
+                N.call("ggnn_shard_merge_wait", allocs[g], epoch & 1, ctypes.c_uint32(epoch), G, m, 10, 10,
+                       *map(N.ptr, out), N.ptr(err), N.stream_ptr())
+                assert int(err.item()) == 0
+                np.testing.assert_array_equal(out[0].cpu().numpy(), ref.ids)
+                np.testing.assert_array_equal(out[1].cpu().numpy(), ref.dists)
+                np.testing.assert_array_equal(out[2].cpu().numpy(), ref.counters)
+    finally:
+        torch.cuda.synchronize()
+        for p in allocs:
+            N.call("ggnn_p2p_free", p)
+
+
 def _group_worker(rank, world, port, q):
     import os
 
@@ -159,7 +217,12 @@ def _group_worker(rank, world, port, q):
         grp = ShardGroup.from_dataset(ga.Dataset(base), ga.BuildConfig(seed=7))
         res = grp.query_arrays(Q, ga.QueryConfig(k_out=10, tau=0.6))
         gt_ids, gt_d = grp.exact_arrays(Q, 10)
-        q.put((rank, res.ids, res.dists, res.counters, gt_ids, gt_d))
+        # the fused exchange (CUDA IPC between the two processes): three
+        # epochs so both parity halves are written and one is reused
+        p2p = [grp.query_arrays(Q, ga.QueryConfig(k_out=10, tau=0.6), exchange="p2p") for _ in range(3)]
+        grp.close()
+        q.put((rank, res.ids, res.dists, res.counters, gt_ids, gt_d,
+               [(r.ids, r.dists, r.counters) for r in p2p]))
     finally:
         dist.destroy_process_group()
 
@@ -191,7 +254,11 @@ def test_shard_group_real_kernels_two_ranks():
     si, _ = ga.build_sharded(ds, 1500, ga.BuildConfig(seed=7))
     ref = ga.query_sharded_arrays(si, Q, ga.QueryConfig(k_out=10, tau=0.6))
     gt = ga.brute_force_oracle(ds, Q, 10)
-    for _, ids, dists, cnt, gi, gd in out:
+    for _, ids, dists, cnt, gi, gd, p2p in out:
+        for pi, pd, pc in p2p:
+            np.testing.assert_array_equal(pi, ref.ids)
+            np.testing.assert_array_equal(pd, ref.dists)
+            np.testing.assert_array_equal(pc, ref.counters)
         np.testing.assert_array_equal(ids, ref.ids)
         np.testing.assert_array_equal(dists, ref.dists)
         np.testing.assert_array_equal(cnt, ref.counters)
