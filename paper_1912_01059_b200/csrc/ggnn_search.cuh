@@ -499,12 +499,58 @@ struct WarpSearch {
         distinct += __popc(__ballot_sync(FULL, ever_insert(lane < nc ? id : -1) != 0));
         check_ever();
       }
-      // candidates are compacted into lanes [0, nc); crow / cid are free now
-      warp_sort_n(key, id, nc, reinterpret_cast<uint64_t*>(crow));
-      const bool adm = lane < nc && KO::to_d(key) <= thr;
-      const int m = __popc(__ballot_sync(FULL, adm));
-      forgotten += nc - m;
-      if (target >= 0) found = __any_sync(FULL, adm && id == target);
+      int m;
+      if (PACK && d <= 33000) {  // u8 keys (d * 255^2) stay below 2^31
+        // admission first, then rank only what is admitted: every rejected
+        // key exceeds thr >= every admitted key, so counting smaller keys
+        // over all nc candidates already ranks the admitted ones among
+        // themselves.  Keys < 2^31: (kj - key) >> 31 == (kj < key).
+        const bool adm = lane < nc && KO::to_d(key) <= thr;
+        const unsigned am = __ballot_sync(FULL, adm);
+        m = __popc(am);
+        forgotten += nc - m;
+        if (target >= 0) found = __any_sync(FULL, adm && id == target);
+        if (m) {
+          uint32_t* ck = reinterpret_cast<uint32_t*>(ckey);
+          if (lane >= nc && lane < ((nc + 3) & ~3)) ck[lane] = 0x7fffffffu;  // never below a real key
+          __syncwarp();
+          int rank = 0;
+          if (adm) {
+            const uint4* k4 = reinterpret_cast<const uint4*>(ck);
+            const uint32_t kk = (uint32_t)key;
+            for (int j = 0; j < nc; j += 4) {
+              const uint4 w = k4[j >> 2];
+              rank += (int)((w.x - kk) >> 31) + (int)((w.y - kk) >> 31) + (int)((w.z - kk) >> 31) +
+                      (int)((w.w - kk) >> 31);
+            }
+          }
+          // equal keys: the smaller id first (the (key, id) order of the ring)
+          const unsigned g = __match_any_sync(FULL, adm ? (uint32_t)key : (0x80000000u | (uint32_t)lane));
+          if (adm && (g & (g - 1u))) {
+            for (unsigned o = g & ~(1u << lane); o; o &= o - 1u) rank += cid[__ffs(o) - 1] < id ? 1 : 0;
+          }
+          __syncwarp();
+          uint64_t* sc = reinterpret_cast<uint64_t*>(crow);  // crow + cid: 32 words
+          if (adm) sc[rank] = pack_ki((uint32_t)key, id);
+          __syncwarp();
+          if (lane < m) {
+            const uint64_t v = sc[lane];
+            key = (Key)(v >> 32);
+            id = (int)(uint32_t)v;
+          } else {
+            key = KO::max_key();
+            id = INT_MAX;
+          }
+          __syncwarp();
+        }
+      } else {
+        // candidates are compacted into lanes [0, nc); crow / cid are free now
+        warp_sort_n(key, id, nc, reinterpret_cast<uint64_t*>(crow));
+        const bool adm = lane < nc && KO::to_d(key) <= thr;
+        m = __popc(__ballot_sync(FULL, adm));
+        forgotten += nc - m;
+        if (target >= 0) found = __any_sync(FULL, adm && id == target);
+      }
       // predict the next expansion -- the smaller of the next unvisited ring
       // entry and the best admitted candidate -- and load its adjacency row
       // while the merge runs (checked against the real head next step)
