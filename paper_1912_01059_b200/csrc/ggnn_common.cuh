@@ -339,7 +339,7 @@ __device__ __forceinline__ void warp_dists(const TX* X, int64_t d, const TQ* qs,
 // LP == 0 keeps the runtime switch above.  LP must equal choose_lpr(...) of
 // the launch; mixed u8-data / float-query searches always use LP == 0.
 #ifndef GGNN_U8_UNR
-#define GGNN_U8_UNR 4  // rows per lane group in flight for 128-byte uint8 rows (8 spills at 80 regs)
+#define GGNN_U8_UNR 3  // row groups in flight for 128-byte uint8 rows: 12 rows ~ the mean candidate count (2 and 4 measured slower)
 #endif
 template <typename TX, typename TQ, int LP>
 __device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
