@@ -669,6 +669,12 @@ SearchCfg make_cfg(const ggnn_search_params* p) {
   return c;
 }
 
+// extra shared memory per CTA (occupancy experiments only: fewer resident
+// searches per SM leave more of the unified L1/shared array to the L1)
+#ifndef GGNN_SMEM_PAD
+#define GGNN_SMEM_PAD 0
+#endif
+
 // choose warps per CTA so that the CTA fits in shared memory
 int pick_warps(size_t region, int want) {
   DevInfo di = dev_info();
@@ -714,7 +720,7 @@ int launch_items(Kern kern, Args a, int64_t items, size_t region, cudaStream_t s
   if (items <= 0) return GGNN_OK;
   int W = pick_warps(region, want);
   GGNN_CHECK_ARG(W > 0, "search state of %zu bytes does not fit in shared memory", region);
-  size_t smem = (size_t)W * region;
+  size_t smem = (size_t)W * region + GGNN_SMEM_PAD;
   GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t grid = (items + W - 1) / W;
   a.work = persistent ? work_counter(st) : nullptr;
