@@ -163,6 +163,13 @@ __device__ __forceinline__ float part_f32_sp(const float4 a, const float* q) {
 #ifndef GGNN_F32_PARTIALS
 #define GGNN_F32_PARTIALS 1
 #endif
+#ifndef GGNN_F32_UNR
+#define GGNN_F32_UNR 4  // float rows in flight per lane group
+#endif
+#ifndef GGNN_F32_CUNR
+#define GGNN_F32_CUNR 1  // unroll of the per-row chunk loop (long float rows)
+#endif
+constexpr int F32_CUNR = GGNN_F32_CUNR;  // (#pragma unroll does not expand macros)
 
 __device__ __forceinline__ double part_f32(const float4 a, const float* q) {
   double d0 = (double)a.x - (double)q[0], d1 = (double)a.y - (double)q[1];
@@ -217,6 +224,7 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
     float accf[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) accf[u] = 0.0f;
+#pragma unroll F32_CUNR
     for (int c = sub; c < nch; c += LPR) {
       float4 v[UNR];
 #pragma unroll
@@ -351,7 +359,7 @@ __device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* q
   } else if constexpr (LP == 8 && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {
     dists_f32_vec<8, 4>(X, d, qs, rows, cnt, kout);
   } else if constexpr (LP == 32 && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {
-    dists_f32_vec<32, 4>(X, d, qs, rows, cnt, kout);
+    dists_f32_vec<32, GGNN_F32_UNR>(X, d, qs, rows, cnt, kout);
   } else {
     warp_dists<TX, TQ>(X, d, qs, rows, cnt, kout, lpr);
   }
