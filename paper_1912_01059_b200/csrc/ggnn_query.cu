@@ -269,6 +269,7 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
   if constexpr (PUSH) {
     __syncwarp();
     push_row(a, qi);
+    __threadfence_system();  // the row is visible to the peers before this warp retires
   }
 }
 
