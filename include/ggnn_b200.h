@@ -121,6 +121,34 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
                      double *d_dists, int32_t *d_counters, void *d_workspace, size_t workspace_bytes,
                      void *stream);
 
+/* ggnn_query_batch over float32 queries that are still being uploaded (the
+ * host-to-host path overlaps the upload with the search): rows
+ * [c * chunk_rows, (c + 1) * chunk_rows) of d_q_f32 may be read once
+ * d_chunk_flags[c] == epoch, which the caller's copy stream writes after the
+ * rows.  narrow != 0 (uint8 tables): rows are narrowed to uint8 on load and a
+ * value that is not an integer in [0, 255] sets bit 0 of *d_status; a chunk
+ * that does not arrive within ~0.5 s sets bit 1.  Either bit voids the
+ * results (the caller reruns).  distinct_touched is not tracked. */
+int ggnn_query_batch_staged(const ggnn_vectors *X, const ggnn_layer *bottom, const int32_t *d_top_rows, int64_t ntop,
+                            const float *d_q_f32, int64_t m, const ggnn_search_params *p, double d_nn1_max,
+                            const uint32_t *d_chunk_flags, int64_t chunk_rows, uint32_t epoch, int32_t narrow,
+                            int32_t *d_ids, double *d_dists, int32_t *d_counters, int32_t *d_status, void *stream);
+
+/* The whole host-to-host query call in one entry: host float32 queries h_q
+ * (pinned for a true async upload) go to d_q_stage in nchunks chunks on
+ * copy_stream, each followed by its flag (the epoch, read from pinned
+ * *h_epoch); ggnn_query_batch_staged searches on search_stream meanwhile and
+ * the results (and status, see above) are copied back into the pinned h_*
+ * buffers on search_stream.  Asynchronous: the caller synchronises both
+ * streams, checks *h_status == 0, and must not change *h_epoch or reuse the
+ * staging buffers before that. */
+int ggnn_query_batch_host(const ggnn_vectors *X, const ggnn_layer *bottom, const int32_t *d_top_rows, int64_t ntop,
+                          const float *h_q, int64_t m, const ggnn_search_params *p, double d_nn1_max, float *d_q_stage,
+                          uint32_t *d_chunk_flags, const uint32_t *h_epoch, int32_t nchunks, int32_t narrow,
+                          int32_t *d_ids, double *d_dists, int32_t *d_counters, int32_t *d_status, int32_t *h_ids,
+                          double *h_dists, int32_t *h_counters, int32_t *h_status, void *search_stream,
+                          void *copy_stream);
+
 /* Replaces: greedy_search (_core.pyx:314-353) for a batch of queries with
  * explicit seeds d_seed_ids / d_seed_dists (m, nseeds; -1 ids skipped). */
 int ggnn_greedy_batch(const ggnn_vectors *X, const ggnn_layer *layer, const ggnn_queries *Q,

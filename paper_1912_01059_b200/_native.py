@@ -96,6 +96,8 @@ _SIGS = {
     "ggnn_query_batch_push": [P, P, P, I64, P, P, F64, P, P, P, P, P],
     "ggnn_p2p_signal": [P, I64, I32, ctypes.c_uint32, P],
     "ggnn_shard_merge_wait": [P, I32, ctypes.c_uint32, I32, I64, I32, I32, P, P, P, P, P],
+    "ggnn_query_batch_staged": [P, P, P, I64, P, I64, P, F64, P, I64, ctypes.c_uint32, I32, P, P, P, P, P],
+    "ggnn_query_batch_host": [P, P, P, I64, P, I64, P, F64, P, P, P, I32, I32, P, P, P, P, P, P, P, P, P, P],
 }
 _RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t,
              "ggnn_layer_stats_scratch_bytes": ctypes.c_size_t, "ggnn_shard_block_bytes": ctypes.c_size_t,

@@ -62,6 +62,13 @@ constexpr int MAX_LAYERS = 24;
 constexpr int SEARCH_WARPS = GGNN_SEARCH_WARPS;
 constexpr int SEARCH_THREADS = 32 * SEARCH_WARPS;
 constexpr int SEARCH_MIN_BLOCKS = GGNN_SEARCH_MIN_BLOCKS;
+// the u8 query kernel fits 64 registers without spills (shared memory still
+// limits it to 28 warps/SM); the staged variant is capped there so its extra
+// load path does not change the search's code generation
+#ifndef GGNN_QUERY_MIN_BLOCKS
+#define GGNN_QUERY_MIN_BLOCKS (32 / GGNN_SEARCH_WARPS)
+#endif
+constexpr int QUERY_MIN_BLOCKS = GGNN_QUERY_MIN_BLOCKS;
 #ifndef GGNN_SYM_PERSISTENT
 #define GGNN_SYM_PERSISTENT 1
 #endif
@@ -123,6 +130,13 @@ struct SearchArgs {
   size_t push_half, push_bb, push_doff, push_coff;
   const int32_t* push_gid;
   int64_t push_gid_size;
+  // queries still arriving (ggnn_query_batch_staged): row qi is usable once
+  // qflags[qi / qchunk] == qepoch; qconv: float rows narrowed to uint8 on load
+  const uint32_t* qflags;
+  int64_t qchunk;
+  uint32_t qepoch;
+  int qconv;
+  int32_t* qstatus;
 };
 
 // Persistent warps: with a work counter (zeroed before the launch) every warp
@@ -142,16 +156,61 @@ __device__ __forceinline__ int64_t next_item(int* work) {
   return (int64_t)__shfl_sync(FULL, v, 0);
 }
 
-template <typename TX, typename TQ>
+// Staged queries: wait (bounded, ~0.5 s) until the host's copy stream has
+// published the chunk holding row qi; a timeout sets bit 1 of *qstatus.
+// The flag is polled with relaxed volatile loads and the row is then read
+// with ld.global.cv (from L2, where the copy landed before the flag): an
+// acquire at system scope would invalidate the SM's L1 at every query start,
+// throwing away the other searches' prefetched rows.
+__device__ __noinline__ void wait_query_chunk(const SearchArgs& a, int64_t qi) {
+  if (lane_id() == 0) {
+    const volatile uint32_t* f = a.qflags + qi / a.qchunk;
+    uint32_t v = *f;
+    if (v != a.qepoch) {
+      const long long t0 = clock64();
+      do {
+        __nanosleep(256);
+        v = *f;
+        if (clock64() - t0 > 1000000000ll) {
+          atomicOr(a.qstatus, 2);
+          break;
+        }
+      } while (v != a.qepoch);
+    }
+  }
+  __syncwarp();
+}
+
+template <typename TX, typename TQ, bool STAGED = false>
 __device__ __forceinline__ void load_query(TQ* qs, const SearchArgs& a, int64_t qi) {
   const int lane = lane_id();
+  if constexpr (STAGED) {
+    wait_query_chunk(a, qi);
+    if (sizeof(TQ) == 1 && a.qconv) {  // float32 row narrowed to uint8 (exact only for integers in [0, 255])
+      const float* src = reinterpret_cast<const float*>(a.Q) + qi * a.d;
+      bool bad = false;
+      for (int64_t e = lane; e < a.d; e += 32) {
+        const float f = __ldcv(src + e);
+        const uint32_t u = (f >= 0.0f && f <= 255.0f) ? (uint32_t)f : 0u;
+        bad |= (float)u != f;
+        qs[e] = (TQ)u;
+      }
+      if (__any_sync(FULL, bad) && lane == 0) atomicOr(a.qstatus, 1);
+      __syncwarp();
+      return;
+    }
+  }
   const TQ* src;
   if (a.qrows) {
     src = reinterpret_cast<const TQ*>(a.X) + (int64_t)__ldg(a.qrows + qi) * a.d;
   } else {
     src = reinterpret_cast<const TQ*>(a.Q) + qi * a.d;
   }
-  for (int64_t e = lane; e < a.d; e += 32) qs[e] = src[e];
+  if constexpr (STAGED) {
+    for (int64_t e = lane; e < a.d; e += 32) qs[e] = __ldcv(src + e);
+  } else {
+    for (int64_t e = lane; e < a.d; e += 32) qs[e] = src[e];
+  }
   __syncwarp();
 }
 
@@ -243,14 +302,14 @@ __device__ __forceinline__ void push_row(const SearchArgs& a, int64_t qi) {
 }
 
 // ------------------------------------------------------------------ query()
-template <typename TX, typename TQ, int LP, bool PUSH = false>
+template <typename TX, typename TQ, int LP, bool PUSH = false, bool STAGED = false>
 __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* smem_w, int* vring_lane, int64_t qi) {
   using Key = typename VecTraits<TX, TQ>::Key;
   const int lane = lane_id();
   WarpSearch<TX, TQ, LP> s;
   s.vr = vring_lane;
   init_search(s, a, smem_w, qi);
-  load_query<TX, TQ>(s.qs, a, qi);
+  load_query<TX, TQ, STAGED>(s.qs, a, qi);
   set_layer(s, a.layer);
   s.dmax = a.dmax;
   s.reset();
@@ -273,17 +332,17 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
   }
 }
 
-template <typename TX, typename TQ, int LP, bool PUSH = false>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
+template <typename TX, typename TQ, int LP, bool PUSH = false, bool STAGED = false>
+__global__ void __launch_bounds__(SEARCH_THREADS, STAGED ? QUERY_MIN_BLOCKS : SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
   if constexpr (GGNN_PERSISTENT != 0) {
     for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
-      query_kernel_one<TX, TQ, LP, PUSH>(a, smem_w, vring_lane, qi);
+      query_kernel_one<TX, TQ, LP, PUSH, STAGED>(a, smem_w, vring_lane, qi);
   } else {
     const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (qi < a.m) query_kernel_one<TX, TQ, LP, PUSH>(a, smem_w, vring_lane, qi);
+    if (qi < a.m) query_kernel_one<TX, TQ, LP, PUSH, STAGED>(a, smem_w, vring_lane, qi);
   }
 }
 
@@ -927,6 +986,90 @@ int ggnn_query_batch_push(const ggnn_vectors* X, const ggnn_layer* bottom, const
       return launch_warps(query_kernel<uint8_t, uint8_t, 0, true>, a, a.m, a.region, st);
     default: return launch_warps(query_kernel<uint8_t, float, 0, true>, a, a.m, a.region, st);
   }
+}
+
+int ggnn_query_batch_staged(const ggnn_vectors* X, const ggnn_layer* bottom, const int32_t* d_top_rows, int64_t ntop,
+                            const float* d_q_f32, int64_t m, const ggnn_search_params* p, double d_nn1_max,
+                            const uint32_t* d_chunk_flags, int64_t chunk_rows, uint32_t epoch, int32_t narrow,
+                            int32_t* d_ids, double* d_dists, int32_t* d_counters, int32_t* d_status, void* stream) {
+  GGNN_CHECK_ARG(X && d_q_f32 && d_chunk_flags && chunk_rows >= 1 && d_status, "invalid staged query arguments");
+  GGNN_CHECK_ARG(!narrow || X->dtype == GGNN_U8, "narrowing needs a uint8 table");
+  ggnn_queries Q;
+  Q.d_data = d_q_f32;
+  Q.d_rows = nullptr;
+  Q.m = m;
+  Q.dtype = narrow ? GGNN_U8 : GGNN_F32;
+  Q.pad_ = 0;
+  SearchArgs a;
+  int rc = fill_common(a, X, &Q, p);
+  if (rc) return rc;
+  GGNN_CHECK_ARG(!(p->flags & GGNN_FLAG_DISTINCT), "the staged search does not track distinct_touched");
+  GGNN_CHECK_ARG(bottom && bottom->d_adj && bottom->k >= 1 && bottom->k <= MAX_K, "invalid bottom layer");
+  GGNN_CHECK_ARG(ntop >= 1, "the top layer is empty");
+  GGNN_CHECK_ARG(d_ids && d_dists && d_counters, "null outputs");
+  a.layer = to_dev(*bottom);
+  a.top_rows = d_top_rows;
+  a.ntop = ntop;
+  a.dmax = d_nn1_max;
+  a.ids = d_ids;
+  a.dists = d_dists;
+  a.counters = d_counters;
+  a.ever_cap = INT_MAX;
+  a.qflags = d_chunk_flags;
+  a.qchunk = chunk_rows;
+  a.qepoch = epoch;
+  a.qconv = narrow ? 1 : 0;
+  a.qstatus = d_status;
+  cudaStream_t st = as_stream(stream);
+  switch (combo(X, &Q)) {
+    case 0:
+      if (a.lpr == 32) return launch_warps(query_kernel<float, float, 32, false, true>, a, a.m, a.region, st);
+      if (a.lpr == 8) return launch_warps(query_kernel<float, float, 8, false, true>, a, a.m, a.region, st);
+      return launch_warps(query_kernel<float, float, 0, false, true>, a, a.m, a.region, st);
+    case 1:
+      if (a.lpr == 32) return launch_warps(query_kernel<uint8_t, uint8_t, 32, false, true>, a, a.m, a.region, st);
+      if (a.lpr == 8) return launch_warps(query_kernel<uint8_t, uint8_t, 8, false, true>, a, a.m, a.region, st);
+      return launch_warps(query_kernel<uint8_t, uint8_t, 0, false, true>, a, a.m, a.region, st);
+    default: return launch_warps(query_kernel<uint8_t, float, 0, false, true>, a, a.m, a.region, st);
+  }
+}
+
+int ggnn_query_batch_host(const ggnn_vectors* X, const ggnn_layer* bottom, const int32_t* d_top_rows, int64_t ntop,
+                          const float* h_q, int64_t m, const ggnn_search_params* p, double d_nn1_max, float* d_q_stage,
+                          uint32_t* d_chunk_flags, const uint32_t* h_epoch, int32_t nchunks, int32_t narrow,
+                          int32_t* d_ids, double* d_dists, int32_t* d_counters, int32_t* d_status, int32_t* h_ids,
+                          double* h_dists, int32_t* h_counters, int32_t* h_status, void* search_stream,
+                          void* copy_stream) {
+  GGNN_CHECK_ARG(X && h_q && d_q_stage && d_chunk_flags && h_epoch && nchunks >= 1 && m >= 1 && h_ids && h_dists &&
+                     h_counters && h_status,
+                 "invalid host query arguments");
+  cudaStream_t ss = as_stream(search_stream), cs = as_stream(copy_stream);
+  const int64_t d = X->d;
+  const int64_t rows = (m + nchunks - 1) / nchunks;
+  const int k = p ? p->k_out : 0;
+  auto upload = [&](int64_t c) -> int {
+    const int64_t lo = c * rows, hi = std::min(m, lo + rows);
+    if (lo >= hi) return GGNN_OK;
+    GGNN_CUDA_TRY(cudaMemcpyAsync(d_q_stage + lo * d, h_q + lo * d, (size_t)(hi - lo) * d * sizeof(float),
+                                  cudaMemcpyHostToDevice, cs));
+    GGNN_CUDA_TRY(cudaMemcpyAsync(d_chunk_flags + c, h_epoch, sizeof(uint32_t), cudaMemcpyHostToDevice, cs));
+    return GGNN_OK;
+  };
+  GGNN_CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t), ss));
+  int rc = upload(0);  // the first chunk is on its way before the search starts
+  if (rc) return rc;
+  rc = ggnn_query_batch_staged(X, bottom, d_top_rows, ntop, d_q_stage, m, p, d_nn1_max, d_chunk_flags, rows, *h_epoch,
+                               narrow, d_ids, d_dists, d_counters, d_status, search_stream);
+  if (rc) return rc;
+  for (int64_t c = 1; c < nchunks; ++c) {
+    rc = upload(c);
+    if (rc) return rc;
+  }
+  GGNN_CUDA_TRY(cudaMemcpyAsync(h_ids, d_ids, (size_t)m * k * sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
+  GGNN_CUDA_TRY(cudaMemcpyAsync(h_dists, d_dists, (size_t)m * k * sizeof(double), cudaMemcpyDeviceToHost, ss));
+  GGNN_CUDA_TRY(cudaMemcpyAsync(h_counters, d_counters, (size_t)m * 5 * sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
+  GGNN_CUDA_TRY(cudaMemcpyAsync(h_status, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
+  return GGNN_OK;
 }
 
 int ggnn_greedy_batch(const ggnn_vectors* X, const ggnn_layer* layer, const ggnn_queries* Q,

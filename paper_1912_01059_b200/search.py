@@ -115,6 +115,12 @@ class _Staging:
         self.dists = N.empty((m, k), t.float64)
         self.cnt = N.empty((m, 5), t.int32)
         self.flag = N.empty((1,), t.int32)
+        # staged path: per-chunk arrival flags (epoch-stamped, never reset)
+        self.chunk_flags = t.zeros((_STAGED_MAX_CHUNKS,), dtype=t.int32, device=N.device())
+        self.epoch = 0
+        self.epoch_pin = t.zeros((1,), dtype=t.int32, pin_memory=True)
+        self.status = N.empty((1,), t.int32)
+        self.status_pin = t.empty((1,), dtype=t.int32, pin_memory=True)
         return self
 
 
@@ -125,11 +131,66 @@ _STAGING: dict = {}
 # streams: chunk i+1's host copy and upload overlap chunk i's search, and
 # chunk i's results come back while later chunks still search
 _CHUNKS = int(__import__("os").environ.get("GGNN_E2E_CHUNKS", "2"))
+# share of the batch in the first chunk (the only upload not hidden behind a search)
+_FIRST = float(__import__("os").environ.get("GGNN_E2E_FIRST", "0.5"))
+# staged path: ONE search launch over the whole batch while the copy stream
+# uploads it chunk by chunk (a warp waits for its chunk's flag), so the batch
+# has one drain instead of one per chunk launch
+_STAGED = __import__("os").environ.get("GGNN_E2E_STAGED", "1") != "0"
+_STAGED_CHUNKS = int(__import__("os").environ.get("GGNN_E2E_STAGED_CHUNKS", "8"))
+_STAGED_MAX_CHUNKS = 64
 _STREAMS: dict = {}
+
+
+def _query_host_staged(dh, Q: np.ndarray, cfg: QueryConfig):
+    """Host arrays in, host arrays out, the upload overlapped with ONE search
+    launch (ggnn_query_batch_staged).  Returns None when the kernel reports a
+    non-integral query on a uint8 table or a chunk that never arrived (the
+    caller then takes the chunked path)."""
+    t = N.torch()
+    dv = dh.vectors
+    m, d = Q.shape
+    k = cfg.k_out
+    dev = t.cuda.current_device()
+    st = _STAGING.setdefault(dev, _Staging()).ensure(m, d, k)
+    streams = _STREAMS.get(dev)
+    if streams is None:
+        streams = _STREAMS[dev] = (t.cuda.Stream(), t.cuda.Stream())
+    main = t.cuda.current_stream()
+    search_s, copy_s = streams
+    nchunks = max(1, min(_STAGED_CHUNKS, _STAGED_MAX_CHUNKS, m // 256))
+    st.epoch = (st.epoch % 0x7FFFFFFF) + 1
+    st.epoch_pin[0] = st.epoch  # no copy of the previous call is pending (it synchronised)
+    params = _params(cfg, _flags(dv, False))
+    narrow = 1 if dv.exact_integers else 0
+    # results land straight in fresh page-locked arrays that the caller keeps
+    # (torch's caching host allocator makes these allocations cheap; the block
+    # returns to its cache when the arrays die): no host-side copy out
+    ids_h = t.empty((m, k), dtype=t.int32, pin_memory=True)
+    dists_h = t.empty((m, k), dtype=t.float64, pin_memory=True)
+    cnt_h = t.empty((m, 5), dtype=t.int32, pin_memory=True)
+    for s_ in streams:
+        s_.wait_stream(main)
+    N.call("ggnn_query_batch_host", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
+           N.ptr(dh.top_rows), dh.ntop, N.P(Q.ctypes.data), m, N.ctypes.byref(params), dh.d_nn1_max,
+           N.ptr(st.q_f32), N.ptr(st.chunk_flags), N.ptr(st.epoch_pin), nchunks, narrow, N.ptr(st.ids),
+           N.ptr(st.dists), N.ptr(st.cnt), N.ptr(st.status), N.ptr(ids_h), N.ptr(dists_h), N.ptr(cnt_h),
+           N.ptr(st.status_pin), N.P(search_s.cuda_stream), N.P(copy_s.cuda_stream))
+    for s_ in streams:
+        main.wait_stream(s_)
+    search_s.synchronize()
+    copy_s.synchronize()
+    if int(st.status_pin[0]) != 0:
+        return None
+    return BatchResult(ids_h.numpy(), dists_h.numpy(), cnt_h.numpy())
 
 
 def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     t = N.torch()
+    if _STAGED and Q.shape[0] >= 1024:
+        r = _query_host_staged(dh, Q, cfg)
+        if r is not None:
+            return r
     dv = dh.vectors
     m, d = Q.shape
     k = cfg.k_out
@@ -141,7 +202,11 @@ def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     main = t.cuda.current_stream()
     params = _params(cfg, _flags(dv, False))
     nchunks = max(1, min(_CHUNKS, m // 1024))
-    bounds = [m * i // nchunks for i in range(nchunks + 1)]
+    if nchunks > 1:
+        first = max(1, min(m - 1, int(m * _FIRST)))
+        bounds = [0] + [first + (m - first) * i // (nchunks - 1) for i in range(nchunks)]
+    else:
+        bounds = [0, m]
     narrow = dv.exact_integers
     if narrow:
         st.flag.fill_(1)

@@ -206,6 +206,40 @@ def test_query_arrays_integral_and_fractional_queries(golden_sift):
     assert same >= 0.98 * len(Qf)
 
 
+def test_staged_host_path_equals_chunked(golden_sift):
+    """The host-to-host path that uploads while ONE launch searches (warps wait
+    for their chunk's flag, rows narrowed in the kernel) answers exactly like
+    the chunked two-stream path, for a ragged batch; a fractional row makes the
+    kernel report it and the call falls back to the float search."""
+    from paper_1912_01059_b200 import search as S
+
+    g, h, queries = golden_sift
+    cfg = ga.QueryConfig(k_out=10, tau=0.6)
+    reps = -(-2731 // len(queries))
+    Q = np.ascontiguousarray(np.tile(queries, (reps, 1))[:2731])
+    assert S._STAGED
+    a = ga.query_arrays(h, Q, cfg)
+    S._STAGED = False
+    try:
+        b = ga.query_arrays(h, Q, cfg)
+    finally:
+        S._STAGED = True
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dists, b.dists)
+    np.testing.assert_array_equal(a.counters, b.counters)
+    np.testing.assert_array_equal(a.ids[: len(queries)], g["q6_ids"])
+    Qf = Q.copy()
+    Qf[1500, 3] += 0.5
+    c = ga.query_arrays(h, Qf, cfg)
+    S._STAGED = False
+    try:
+        d = ga.query_arrays(h, Qf, cfg)
+    finally:
+        S._STAGED = True
+    np.testing.assert_array_equal(c.ids, d.ids)
+    np.testing.assert_array_equal(c.dists, d.dists)
+
+
 def test_distinct_touched_exact_past_compact_table(golden_sift):
     """Searches that touch more ids than the compact distinct-set holds
     (3/4 of 4096) are rerun with exact tables: distinct_touched (and every
