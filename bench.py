@@ -344,6 +344,13 @@ def main():
     base, Q = make_workload(args)
     ds = ga.Dataset(base)
     cfg = ga.BuildConfig(seed=7)
+    # warm process: one small build first loads the kernels and grows the
+    # allocators, so build_seconds is the index build itself
+    warm_n = min(args.n // 4, 50_000)
+    t_w = time.perf_counter()
+    ga.build(ga.Dataset(np.ascontiguousarray(base[:warm_n])), cfg)
+    torch.cuda.synchronize()
+    warmup_build_s = time.perf_counter() - t_w
     dist.barrier()
     h, bstats = ga.build(ds, cfg)
     build_s = dist.max(bstats.build_seconds)
@@ -495,6 +502,8 @@ def main():
                    "tau": tau, "recall": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
                    "mean_visited": chosen["V"], "mean_steps": chosen["T"], "tau_sweep": sweep,
                    "build_seconds": build_s, "ground_truth_seconds": gt_s,
+                   "build_note": f"warm process: a {warm_n}-point build ran first ({warmup_build_s:.2f} s, module "
+                                 f"loading and allocator growth); build_seconds = the full index build after it",
                    "build_phase_seconds_top": dict(sorted(
                        bstats.phase_seconds.items(), key=lambda kv: -kv[1])[:6]),
                    "two_batches_in_flight": pipelined,
@@ -546,6 +555,8 @@ def run_sharded(args, dist, ga, torch):
     _, Q = make_latent16(n=args.n, d=args.d, m=args.queries, seed=1234)
     base = make_latent16_shard(n=args.n, d=args.d, shard=r, seed=1234)
     ds = ga.Dataset(base)
+    ga.build(ga.Dataset(np.ascontiguousarray(base[:min(args.n // 4, 50_000)])), ga.BuildConfig(seed=7))  # warm
+    torch.cuda.synchronize()
     dist.barrier()
     h, bstats = ga.build(ds, ga.BuildConfig(seed=7))
     build_s = dist.max(bstats.build_seconds)

@@ -97,26 +97,33 @@ def select_segments(weights: np.ndarray, seg_offsets: np.ndarray, quotas: np.nda
     """Vectorised select_points over consecutive segments: identical output
     to calling select_points(weights[lo:hi], quota, rng) segment by segment
     (one rng.random(total) draw equals the per-segment draws concatenated).
-    Returns the chosen positions (into `weights`), ascending per segment."""
+    Returns the chosen positions (into `weights`), ascending per segment.
+    Segments are laid out as rows of a padded matrix and sorted row-wise
+    (stable, descending key: ties keep position order, like the reference's
+    stable argsort, _purepy.py:42 / build.py:120)."""
     weights = np.asarray(weights, dtype=np.float64)
     total = len(weights)
     u = rng.random(total)
+    seg_offsets = np.asarray(seg_offsets, dtype=np.int64)
     nseg = len(seg_offsets) - 1
+    if nseg <= 0 or total == 0:
+        return np.zeros(0, dtype=np.int64)
     sizes = np.diff(seg_offsets)
+    starts = seg_offsets[:-1]
     seg_id = np.repeat(np.arange(nseg), sizes)
-    pos_pos = weights > 0
+    nz = sizes > 0
     any_pos = np.zeros(nseg, dtype=bool)
-    np.logical_or.at(any_pos, seg_id, pos_pos)
+    any_pos[nz] = np.maximum.reduceat((weights > 0).astype(np.int8), starts[nz]) > 0
     with np.errstate(divide="ignore", invalid="ignore"):
         keys = np.where(any_pos[seg_id], np.log(u) / weights, u)
-    idx = np.arange(total)
-    # stable descending key order within each segment: sort by (segment, -key, index)
-    order = np.lexsort((idx, -keys, seg_id))
-    ordered_seg = seg_id[order]
-    first = np.searchsorted(ordered_seg, np.arange(nseg), side="left")
-    within = idx - first[ordered_seg]
-    chosen = order[within < np.asarray(quotas)[ordered_seg]]
-    return chosen[np.lexsort((chosen, seg_id[chosen]))]
+    width = int(sizes.max())
+    pad = np.full((nseg, width), np.inf)  # padding sorts after every real key (stable)
+    pad[seg_id, np.arange(total) - starts[seg_id]] = -keys
+    order = np.argsort(pad, axis=1, kind="stable")
+    take = np.arange(width)[None, :] < np.minimum(np.asarray(quotas, dtype=np.int64), sizes)[:, None]
+    rows, cols = np.nonzero(take)
+    chosen = starts[rows] + order[rows, cols]
+    return chosen[np.lexsort((chosen, rows))]
 
 
 def _segment_of(h, layer_index: int, node: int) -> int:
