@@ -121,7 +121,8 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
                      double *d_dists, int32_t *d_counters, void *d_workspace, size_t workspace_bytes,
                      void *stream);
 
-/* ggnn_query_batch over float32 queries that are still being uploaded (the
+/* Replaces: query (search.py:115-137) for a batch, like ggnn_query_batch,
+ * over float32 queries that are still being uploaded (the
  * host-to-host path overlaps the upload with the search): rows
  * [c * chunk_rows, (c + 1) * chunk_rows) of d_q_f32 may be read once
  * d_chunk_flags[c] == epoch, which the caller's copy stream writes after the
@@ -134,7 +135,8 @@ int ggnn_query_batch_staged(const ggnn_vectors *X, const ggnn_layer *bottom, con
                             const uint32_t *d_chunk_flags, int64_t chunk_rows, uint32_t epoch, int32_t narrow,
                             int32_t *d_ids, double *d_dists, int32_t *d_counters, int32_t *d_status, void *stream);
 
-/* The whole host-to-host query call in one entry: host float32 queries h_q
+/* Replaces: batch_query (search.py:213-226) called with host arrays, as one
+ * asynchronous native call.  The whole host-to-host query: host float32 queries h_q
  * (pinned for a true async upload) go to d_q_stage in nchunks chunks on
  * copy_stream, each followed by its flag (the epoch, read from pinned
  * *h_epoch); ggnn_query_batch_staged searches on search_stream meanwhile and

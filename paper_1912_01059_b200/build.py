@@ -34,7 +34,7 @@ SYM_FALLBACK = 8
 # approximate that order (later windows see earlier windows' updates).  Small
 # layers take fine windows (cheap, and where single links matter most:
 # tests/golden/deep3k); large layers 16 (each window still fills the GPU).
-SMALL_LAYER = 200_000
+SMALL_LAYER = int(__import__("os").environ.get("GGNN_SMALL_LAYER", "200000"))
 _ENV = __import__("os").environ
 
 

@@ -20,3 +20,14 @@ for k, v in ph.items():
     groups[kind] = groups.get(kind, 0.0) + v
 for k, v in sorted(groups.items(), key=lambda kv: -kv[1]):
     print(f"{k:10s} {v:7.3f} s")
+by_layer = {}
+for k, v in ph.items():
+    parts = k.split("/")
+    j = None
+    for p_ in parts[1:]:
+        if p_.startswith("merge") or p_.startswith("refine"):
+            j = int(p_.replace("merge", "").replace("refine", "").split(".")[0])
+    key = f"layer {j}" if j is not None else parts[-1]
+    by_layer[key] = by_layer.get(key, 0.0) + v
+for k, v in sorted(by_layer.items(), key=lambda kv: -kv[1]):
+    print(f"{k:10s} {v:7.3f} s")
