@@ -240,6 +240,31 @@ def test_staged_host_path_equals_chunked(golden_sift):
     np.testing.assert_array_equal(c.dists, d.dists)
 
 
+def test_staged_host_path_float_table():
+    """The staged host path on a float table (no narrowing): equal to the
+    chunked path and to the device-resident call."""
+    from paper_1912_01059_b200 import search as S
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, Q = make_latent16(n=6000, d=64, m=1500, seed=11)
+    ds = ga.Dataset((base / 255.0).astype(np.float32))
+    Qf = (Q / 255.0).astype(np.float32)
+    h, _ = ga.build(ds, ga.BuildConfig(seed=7))
+    cfg = ga.QueryConfig(k_out=10, tau=0.5)
+    a = ga.query_arrays(h, Qf, cfg)
+    S._STAGED = False
+    try:
+        b = ga.query_arrays(h, Qf, cfg)
+    finally:
+        S._STAGED = True
+    ids, dists, cnt = ga.query_arrays(h, Qf, cfg, out="device")
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dists, b.dists)
+    np.testing.assert_array_equal(a.counters, b.counters)
+    np.testing.assert_array_equal(a.ids, ids.cpu().numpy())
+    np.testing.assert_array_equal(a.dists, dists.cpu().numpy())
+
+
 def test_distinct_touched_exact_past_compact_table(golden_sift):
     """Searches that touch more ids than the compact distinct-set holds
     (3/4 of 4096) are rerun with exact tables: distinct_touched (and every
