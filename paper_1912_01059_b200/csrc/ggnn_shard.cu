@@ -167,11 +167,18 @@ extern "C" size_t ggnn_p2p_bytes(int32_t G, int64_t m, int32_t k) { return 2 * p
 extern "C" int ggnn_p2p_alloc(size_t bytes, void** d_ptr, void* ipc_handle_out) {
   GGNN_CHECK_ARG(d_ptr && ipc_handle_out && bytes > 0, "ggnn_p2p_alloc: invalid arguments");
   static_assert(sizeof(cudaIpcMemHandle_t) == GGNN_IPC_HANDLE_BYTES, "IPC handle size");
-  GGNN_CUDA_TRY(cudaMalloc(d_ptr, bytes));
-  GGNN_CUDA_TRY(cudaMemset(*d_ptr, 0, bytes));
+  void* p = nullptr;
+  GGNN_CUDA_TRY(cudaMalloc(&p, bytes));
   cudaIpcMemHandle_t h;
-  GGNN_CUDA_TRY(cudaIpcGetMemHandle(&h, *d_ptr));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);  // no leak on the error path
+    ::ggnn::set_error("ggnn_p2p_alloc: %s", cudaGetErrorString(e));
+    return GGNN_E_CUDA;
+  }
   memcpy(ipc_handle_out, &h, sizeof(h));
+  *d_ptr = p;
   return GGNN_OK;
 }
 
