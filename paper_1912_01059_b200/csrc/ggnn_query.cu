@@ -69,6 +69,10 @@ constexpr int SEARCH_MIN_BLOCKS = GGNN_SEARCH_MIN_BLOCKS;
 #define GGNN_QUERY_MIN_BLOCKS (32 / GGNN_SEARCH_WARPS)
 #endif
 constexpr int QUERY_MIN_BLOCKS = GGNN_QUERY_MIN_BLOCKS;
+#ifndef GGNN_STAGED_CAP
+#define GGNN_STAGED_CAP 1
+#endif
+constexpr bool STAGED_CAP = GGNN_STAGED_CAP != 0;
 #ifndef GGNN_SYM_PERSISTENT
 #define GGNN_SYM_PERSISTENT 1
 #endif
@@ -162,7 +166,7 @@ __device__ __forceinline__ int64_t next_item(int* work) {
 // with ld.global.cv (from L2, where the copy landed before the flag): an
 // acquire at system scope would invalidate the SM's L1 at every query start,
 // throwing away the other searches' prefetched rows.
-__device__ __noinline__ void wait_query_chunk(const SearchArgs& a, int64_t qi) {
+__device__ __forceinline__ void wait_query_chunk(const SearchArgs& a, int64_t qi) {
   if (lane_id() == 0) {
     const volatile uint32_t* f = a.qflags + qi / a.qchunk;
     uint32_t v = *f;
@@ -333,7 +337,9 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
 }
 
 template <typename TX, typename TQ, int LP, bool PUSH = false, bool STAGED = false>
-__global__ void __launch_bounds__(SEARCH_THREADS, STAGED ? QUERY_MIN_BLOCKS : SEARCH_MIN_BLOCKS) query_kernel(const __grid_constant__ SearchArgs a) {
+__global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeof(TX) == 1) ? QUERY_MIN_BLOCKS
+                                                                                              : SEARCH_MIN_BLOCKS)
+    query_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;

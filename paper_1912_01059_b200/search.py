@@ -187,7 +187,9 @@ def _query_host_staged(dh, Q: np.ndarray, cfg: QueryConfig):
 
 def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     t = N.torch()
-    if _STAGED and Q.shape[0] >= 1024:
+    # staged: uint8 tables only (float32 rows stay float and their upload is
+    # 4x larger; measured slower than the chunked path on gist1m)
+    if _STAGED and Q.shape[0] >= 1024 and dh.vectors.exact_integers:
         r = _query_host_staged(dh, Q, cfg)
         if r is not None:
             return r

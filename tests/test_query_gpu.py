@@ -241,8 +241,9 @@ def test_staged_host_path_equals_chunked(golden_sift):
 
 
 def test_staged_host_path_float_table():
-    """The staged host path on a float table (no narrowing): equal to the
-    chunked path and to the device-resident call."""
+    """Float tables take the chunked host path (the staged one is for uint8
+    tables): with and without the staged switch, equal to the
+    device-resident call."""
     from paper_1912_01059_b200 import search as S
     from paper_1912_01059_b200.synthetic import make_latent16
 
