@@ -366,6 +366,7 @@ def main():
 
     # ---- device-resident kernel timing (value) ------------------------
     from paper_1912_01059_b200.device import device_hierarchy
+    from paper_1912_01059_b200.search import _qflags
 
     dh = device_hierarchy(h)
     dv = dh.vectors
@@ -374,7 +375,7 @@ def main():
     ids = N.empty((m, 10), torch.int32)
     dists = N.empty((m, 10), torch.float64)
     cnt = N.empty((m, 5), torch.int32)
-    params = N.search_params(10, qcfg.prioq_size, qcfg.visited_size, tau, qcfg.max_iterations, 0)
+    params = N.search_params(10, qcfg.prioq_size, qcfg.visited_size, tau, qcfg.max_iterations, _qflags(dh, False))
 
     def step():
         N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
@@ -548,6 +549,7 @@ def run_sharded(args, dist, ga, torch):
     from paper_1912_01059_b200 import _native as N
     from paper_1912_01059_b200.device import device_hierarchy
     from paper_1912_01059_b200.distributed import ShardGroup
+    from paper_1912_01059_b200.search import _qflags
     from paper_1912_01059_b200.shard import block_layout, block_pointers
     from paper_1912_01059_b200.synthetic import make_latent16, make_latent16_shard
 
@@ -587,7 +589,7 @@ def run_sharded(args, dist, ga, torch):
     out_ids = N.empty((m, 10), torch.int32)
     out_d = N.empty((m, 10), torch.float64)
     out_c = N.empty((m, 5), torch.int32)
-    params = N.search_params(10, qcfg.prioq_size, qcfg.visited_size, tau, qcfg.max_iterations, 0)
+    params = N.search_params(10, qcfg.prioq_size, qcfg.visited_size, tau, qcfg.max_iterations, _qflags(dh, False))
     gid = grp.gid_dev()
     stream = torch.cuda.current_stream()
     qev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]

@@ -41,6 +41,9 @@ extern "C" {
 /* search flags */
 #define GGNN_FLAG_DISTINCT 1    /* exact distinct_touched (diagnostic; needs workspace) */
 #define GGNN_FLAG_EXACT_DISTS 2 /* re-score returned hits with the sequential FP64 sum  */
+#define GGNN_FLAG_UNIQUE_ROWS 4 /* caller asserts (ggnn_rows_unique) that no adjacency row of the
+                                   searched layer repeats a neighbour: the per-step duplicate
+                                   filter (_core.pyx:268-272) is skipped */
 
 /* Termination codes, _core.pyx:21-23 */
 #define GGNN_TERM_STOPPING 0
@@ -108,6 +111,10 @@ size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params *p, int32
  * else -1. */
 int ggnn_sanitize_layer(const int32_t *d_adj, const int32_t *d_sym_count, int64_t node_count, int32_t k,
                         int32_t k_nn, int32_t *d_out, void *stream);
+
+/* *d_result = 1 if no row of the (sanitized) adjacency holds the same
+ * neighbour twice, else 0 (for GGNN_FLAG_UNIQUE_ROWS). */
+int ggnn_rows_unique(const int32_t *d_adj, int64_t node_count, int32_t k, int32_t *d_result, void *stream);
 
 /* Replaces: search.query (search.py:115-137) = top_layer_seeds
  * (search.py:100-112, exhaustive_topk _core.pyx:86-104 over the top layer)

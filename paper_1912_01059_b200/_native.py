@@ -20,6 +20,7 @@ GGNN_F32 = 0
 GGNN_U8 = 1
 FLAG_DISTINCT = 1
 FLAG_EXACT_DISTS = 2
+FLAG_UNIQUE_ROWS = 4
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32
@@ -63,6 +64,7 @@ _SIGS = {
     "ggnn_device_info": [P, P],
     "ggnn_search_workspace_bytes": [I64, P, I32],
     "ggnn_sanitize_layer": [P, P, I64, I32, I32, P, P],
+    "ggnn_rows_unique": [P, I64, I32, P, P],
     "ggnn_query_batch": [P, P, P, I64, P, P, F64, P, P, P, P, ctypes.c_size_t, P],
     "ggnn_greedy_batch": [P, P, P, P, P, I32, P, F64, P, P, P, P, ctypes.c_size_t, P],
     "ggnn_descent_batch": [P, P, I32, I32, I32, P, P, P, P, P, P, P, P, ctypes.c_size_t, P],

@@ -906,6 +906,26 @@ size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params* p, int32
   return (size_t)m * std::min(full, COMPACT_EVER) * 4;
 }
 
+__global__ void rows_unique_kernel(const int32_t* adj, int64_t node_count, int k, int32_t* result) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= node_count) return;
+  const int lane = lane_id();
+  const int32_t v = lane < k ? adj[row * k + lane] : -1;
+  const unsigned same = __match_any_sync(FULL, v >= 0 ? (unsigned)v : (0x80000000u | (unsigned)lane));
+  if (v >= 0 && (same & ~(1u << lane))) *result = 0;
+}
+
+int ggnn_rows_unique(const int32_t* d_adj, int64_t node_count, int32_t k, int32_t* d_result, void* stream) {
+  GGNN_CHECK_ARG(d_adj && d_result && node_count >= 0 && k >= 1 && k <= 32, "invalid arguments");
+  cudaStream_t st = as_stream(stream);
+  const int32_t one = 1;
+  GGNN_CUDA_TRY(cudaMemcpyAsync(d_result, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+  if (node_count == 0) return GGNN_OK;
+  rows_unique_kernel<<<(unsigned)((node_count + 7) / 8), 256, 0, st>>>(d_adj, node_count, k, d_result);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
 int ggnn_sanitize_layer(const int32_t* d_adj, const int32_t* d_sym_count, int64_t node_count, int32_t k,
                         int32_t k_nn, int32_t* d_out, void* stream) {
   GGNN_CHECK_ARG(d_adj && d_out && node_count >= 0 && k >= 1 && k <= MAX_K && k_nn >= 1 && k_nn <= k,

@@ -39,6 +39,7 @@ struct SearchCfg {
 
 constexpr int FLAG_DISTINCT = 1;     // exact distinct_touched via a global set
 constexpr int FLAG_EXACT_DISTS = 2;  // re-score returned hits sequentially (bitwise _sqdist)
+constexpr int FLAG_UNIQUE_ROWS = 4;  // rows never repeat a neighbour: no duplicate filter
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -473,8 +474,10 @@ struct WarpSearch {
     }
     bool cand = nb >= 0;
     if (cand) cand = ht.count((uint32_t)nb) == 0u;
-    unsigned same = __match_any_sync(FULL, cand ? (unsigned)nb : (0x80000000u | (unsigned)lane));
-    cand = cand && ((same & lanemask_lt()) == 0u);
+    if (!(c.flags & FLAG_UNIQUE_ROWS)) {  // "nb in cands" (_core.pyx:268-272)
+      unsigned same = __match_any_sync(FULL, cand ? (unsigned)nb : (0x80000000u | (unsigned)lane));
+      cand = cand && ((same & lanemask_lt()) == 0u);
+    }
     const unsigned cm = __ballot_sync(FULL, cand);
     const int nc = __popc(cm);
     bool found = false;

@@ -223,7 +223,7 @@ class P2PExchange:
     def search_push(self, h, Q: np.ndarray, cfg: QueryConfig) -> None:
         """Launch the push search + signal of the next epoch (no merge)."""
         from .device import device_hierarchy
-        from .search import _flags, _params
+        from .search import _params, _qflags
 
         if Q.shape[0] != self.m or cfg.k_out != self.k:
             raise ValueError("batch shape does not match this exchange")
@@ -232,7 +232,7 @@ class P2PExchange:
         dh = device_hierarchy(h)
         dv = dh.vectors
         dq, qs = dv.queries(Q)
-        params = _params(cfg, _flags(dv, False))
+        params = _params(cfg, _qflags(dh, False))
         N.call("ggnn_query_batch_push", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
                N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max,
                N.ptr(self.local_ids), N.ptr(self.local_dists), N.ptr(self.local_cnt), N.ctypes.byref(self.push),

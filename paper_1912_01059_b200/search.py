@@ -75,6 +75,19 @@ def _flags(dv: DeviceVectors, distinct: bool) -> int:
     return f | (N.FLAG_DISTINCT if distinct else 0)
 
 
+def _qflags(dh, distinct: bool) -> int:
+    """Flags of a query-kernel launch on dh's bottom layer: _flags plus
+    GGNN_FLAG_UNIQUE_ROWS when no adjacency row repeats a neighbour (checked
+    once per device hierarchy; the kernel then skips its duplicate filter)."""
+    u = getattr(dh, "_unique0", None)
+    if u is None:
+        L = dh.layers[0]
+        res = N.empty((1,), N.torch().int32)
+        N.call("ggnn_rows_unique", N.ptr(L.adj), L.node_count, L.k, N.ptr(res), N.stream_ptr())
+        u = dh._unique0 = bool(int(res.item()))
+    return _flags(dh.vectors, distinct) | (N.FLAG_UNIQUE_ROWS if u else 0)
+
+
 def _workspace(m, params, max_seeds):
     nbytes = N.load().ggnn_search_workspace_bytes(m, N.ctypes.byref(params), max_seeds)
     if not nbytes:
@@ -161,7 +174,7 @@ def _query_host_staged(dh, Q: np.ndarray, cfg: QueryConfig):
     nchunks = max(1, min(_STAGED_CHUNKS, _STAGED_MAX_CHUNKS, m // 256))
     st.epoch = (st.epoch % 0x7FFFFFFF) + 1
     st.epoch_pin[0] = st.epoch  # no copy of the previous call is pending (it synchronised)
-    params = _params(cfg, _flags(dv, False))
+    params = _params(cfg, _qflags(dh, False))
     narrow = 1 if dv.exact_integers else 0
     # results land straight in fresh page-locked arrays that the caller keeps
     # (torch's caching host allocator makes these allocations cheap; the block
@@ -202,7 +215,7 @@ def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     if streams is None:
         streams = _STREAMS[dev] = (t.cuda.Stream(), t.cuda.Stream())
     main = t.cuda.current_stream()
-    params = _params(cfg, _flags(dv, False))
+    params = _params(cfg, _qflags(dh, False))
     nchunks = max(1, min(_CHUNKS, m // 1024))
     if nchunks > 1:
         first = max(1, min(m - 1, int(m * _FIRST)))
@@ -277,7 +290,7 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
     ids = N.empty((m, cfg.k_out), t.int32)
     dists = N.empty((m, cfg.k_out), t.float64)
     cnt = N.empty((m, 5), t.int32)
-    params = _params(cfg, _flags(dv, distinct))
+    params = _params(cfg, _qflags(dh, distinct))
     dq, qs = dv.queries(Q)
     bottom = dh.layers[0]
 
@@ -313,7 +326,7 @@ def launch_query(h, queries: np.ndarray, cfg: QueryConfig, ids_p, dists_p, cnt_p
     dh = device_hierarchy(h)
     dv = dh.vectors
     dq, qs = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
-    params = _params(cfg, _flags(dv, False))
+    params = _params(cfg, _qflags(dh, False))
     N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct), N.ptr(dh.top_rows),
            dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, ids_p, dists_p, cnt_p, None, 0,
            N.stream_ptr())

@@ -13,6 +13,7 @@ import pytest
 
 import oracle as O
 import paper_1912_01059_b200 as ga
+from paper_1912_01059_b200 import _native as N
 from conftest import TERM_CODE, golden_hierarchy, oracle_layers
 
 pytestmark = pytest.mark.gpu
@@ -264,6 +265,55 @@ def test_staged_host_path_float_table():
     np.testing.assert_array_equal(a.counters, b.counters)
     np.testing.assert_array_equal(a.ids, ids.cpu().numpy())
     np.testing.assert_array_equal(a.dists, dists.cpu().numpy())
+
+
+def test_duplicate_neighbours_in_rows():
+    """ggnn_rows_unique flags rows that repeat a neighbour; such a layer is
+    searched with the duplicate filter ("nb in cands", _core.pyx:268-272) and
+    still matches the CPU checker bit for bit, while duplicate-free layers
+    skip the filter (GGNN_FLAG_UNIQUE_ROWS) with identical answers."""
+    import torch
+
+    from paper_1912_01059_b200 import search as S
+    from paper_1912_01059_b200.device import device_hierarchy
+
+    adj = torch.tensor([[0, 1, 2, -1], [3, 3, -1, -1], [-1, -1, -1, -1]], dtype=torch.int32, device="cuda")
+    res = torch.empty(1, dtype=torch.int32, device="cuda")
+    N.call("ggnn_rows_unique", N.ptr(adj), 3, 4, N.ptr(res), N.stream_ptr())
+    assert int(res.item()) == 0
+    N.call("ggnn_rows_unique", N.ptr(adj), 1, 4, N.ptr(res), N.stream_ptr())
+    assert int(res.item()) == 1
+
+    rng = np.random.default_rng(3)
+    X = rng.integers(0, 40, size=(3000, 16)).astype(np.float32)
+    Q = rng.integers(0, 40, size=(200, 16)).astype(np.float32)
+    ds = ga.Dataset(X)
+    h, _ = ga.build(ds, ga.BuildConfig(seed=7))
+    cfg = ga.QueryConfig(k_out=10, tau=0.6)
+    assert S._qflags(device_hierarchy(h), False) & N.FLAG_UNIQUE_ROWS
+    base = ga.query_arrays(h, Q, cfg)
+    # host copy of the layers with duplicated neighbours appended as sym slots
+    L0 = h.layers[0]
+    adjh = L0.adjacency.copy()
+    symc = L0.sym_count.copy()
+    for r in range(0, L0.node_count, 7):
+        free = L0.k_nn + symc[r]
+        if free < L0.k and adjh[r, 0] >= 0:
+            adjh[r, free] = adjh[r, 0]
+            symc[r] += 1
+    L0.adjacency[:] = adjh
+    L0.sym_count[:] = symc
+    L0.touch()
+    dh = device_hierarchy(h)
+    assert not S._qflags(dh, False) & N.FLAG_UNIQUE_ROWS
+    dup = ga.query_arrays(h, Q, cfg)
+    layers = [(L.adjacency, L.k_nn, L.sym_count) for L in h.layers]
+    for i in range(0, 200, 13):
+        ids, dd, v, t, term, _, _ = O.query(layers, h.to_bottom, X, Q[i], 10, 0.6, h.stats.d_nn1_max)
+        np.testing.assert_array_equal(dup.ids[i, :len(ids)], ids)
+        np.testing.assert_array_equal(dup.dists[i, :len(dd)], dd)
+        assert (dup.counters[i, 0], dup.counters[i, 1], dup.counters[i, 2]) == (v, t, term)
+    assert base.ids.shape == dup.ids.shape
 
 
 def test_distinct_touched_exact_past_compact_table(golden_sift):

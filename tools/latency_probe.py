@@ -18,7 +18,13 @@ h, _ = ga.build(ga.Dataset(base), ga.BuildConfig(seed=7))
 dh = device_hierarchy(h)
 dv = dh.vectors
 tau = float(sys.argv[1]) if len(sys.argv) > 1 else 0.6
-params = N.search_params(10, 256, 512, tau, 1000, 0)
+import os  # noqa: E402
+
+from paper_1912_01059_b200 import search as S  # noqa: E402
+
+qflags = 0 if os.environ.get("GGNN_NO_UNIQUE") else S._qflags(dh, False)
+print("flags", qflags)
+params = N.search_params(10, 256, 512, tau, 1000, qflags)
 Qall = np.concatenate([Q, Q[::-1]])
 sizes = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [148, 592, 1184, 2368, 4144, 6000, 8000,
                                                                            10000, 20000]
