@@ -517,20 +517,21 @@ struct WarpSearch {
           uint32_t* ck = reinterpret_cast<uint32_t*>(ckey);
           if (lane >= nc && lane < ((nc + 3) & ~3)) ck[lane] = 0x7fffffffu;  // never below a real key
           __syncwarp();
-          int rank = 0;
+          int rank = 0, eq = 0;
+          const uint32_t kk = (uint32_t)key;
           if (adm) {
             const uint4* k4 = reinterpret_cast<const uint4*>(ck);
-            const uint32_t kk = (uint32_t)key;
             for (int j = 0; j < nc; j += 4) {
               const uint4 w = k4[j >> 2];
               rank += (int)((w.x - kk) >> 31) + (int)((w.y - kk) >> 31) + (int)((w.z - kk) >> 31) +
                       (int)((w.w - kk) >> 31);
+              eq += (int)(w.x == kk) + (int)(w.y == kk) + (int)(w.z == kk) + (int)(w.w == kk);
             }
           }
-          // equal keys: the smaller id first (the (key, id) order of the ring)
-          const unsigned g = __match_any_sync(FULL, adm ? (uint32_t)key : (0x80000000u | (uint32_t)lane));
-          if (adm && (g & (g - 1u))) {
-            for (unsigned o = g & ~(1u << lane); o; o &= o - 1u) rank += cid[__ffs(o) - 1] < id ? 1 : 0;
+          // equal keys (only admitted ones can equal an admitted key): the
+          // smaller id first, the (key, id) order of the ring; eq counts self
+          if (adm && eq > 1) {
+            for (int j = 0; j < nc; ++j) rank += (ck[j] == kk && cid[j] < id) ? 1 : 0;
           }
           __syncwarp();
           uint64_t* sc = reinterpret_cast<uint64_t*>(crow);  // crow + cid: 32 words
