@@ -16,7 +16,7 @@ for s in $stages; do
     bench)
       timeout 1200 python bench.py --steps 20 --warmup 3 --out gpurun_out/bench.json > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -c 3000 gpurun_out/bench.log ;;
     launches)
-      timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+      timeout 2700 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
         python bench.py --steps 3 --warmup 3 --tau ${TAU:-0.55} --no-cpu-baseline > gpurun_out/launches.log 2>&1; echo "launches rc=$?" ;;
     ncu)
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:query_kernel -s 2 -c 1 -f \
