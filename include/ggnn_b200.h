@@ -135,7 +135,7 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
  * d_chunk_flags[c] == epoch, which the caller's copy stream writes after the
  * rows.  narrow != 0 (uint8 tables): rows are narrowed to uint8 on load and a
  * value that is not an integer in [0, 255] sets bit 0 of *d_status; a chunk
- * that does not arrive within ~0.5 s sets bit 1.  Either bit voids the
+ * that does not arrive within ~50 ms sets bit 1.  Either bit voids the
  * results (the caller reruns).  distinct_touched is not tracked. */
 int ggnn_query_batch_staged(const ggnn_vectors *X, const ggnn_layer *bottom, const int32_t *d_top_rows, int64_t ntop,
                             const float *d_q_f32, int64_t m, const ggnn_search_params *p, double d_nn1_max,
@@ -146,8 +146,9 @@ int ggnn_query_batch_staged(const ggnn_vectors *X, const ggnn_layer *bottom, con
  * asynchronous native call.  The whole host-to-host query: host float32 queries h_q
  * (pinned for a true async upload) go to d_q_stage in nchunks chunks on
  * copy_stream, each followed by its flag (the epoch, read from pinned
- * *h_epoch); ggnn_query_batch_staged searches on search_stream meanwhile and
- * the results (and status, see above) are copied back into the pinned h_*
+ * *h_epoch), all queued before ggnn_query_batch_staged is launched on
+ * search_stream (which then overlaps the chunks still in flight); the
+ * results (and status, see above) are copied back into the pinned h_*
  * buffers on search_stream.  Asynchronous: the caller synchronises both
  * streams, checks *h_status == 0, and must not change *h_epoch or reuse the
  * staging buffers before that. */

@@ -160,7 +160,7 @@ __device__ __forceinline__ int64_t next_item(int* work) {
   return (int64_t)__shfl_sync(FULL, v, 0);
 }
 
-// Staged queries: wait (bounded, ~0.5 s) until the host's copy stream has
+// Staged queries: wait (bounded, ~50 ms) until the host's copy stream has
 // published the chunk holding row qi; a timeout sets bit 1 of *qstatus.
 // The flag is polled with relaxed volatile loads and the row is then read
 // with ld.global.cv (from L2, where the copy landed before the flag): an
@@ -175,7 +175,7 @@ __device__ __forceinline__ void wait_query_chunk(const SearchArgs& a, int64_t qi
       do {
         __nanosleep(256);
         v = *f;
-        if (clock64() - t0 > 1000000000ll) {
+        if (clock64() - t0 > 100000000ll) {  // ~50 ms: the chunk was queued before the launch
           atomicOr(a.qstatus, 2);
           break;
         }
@@ -1082,15 +1082,18 @@ int ggnn_query_batch_host(const ggnn_vectors* X, const ggnn_layer* bottom, const
     return GGNN_OK;
   };
   GGNN_CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t), ss));
-  int rc = upload(0);  // the first chunk is on its way before the search starts
-  if (rc) return rc;
-  rc = ggnn_query_batch_staged(X, bottom, d_top_rows, ntop, d_q_stage, m, p, d_nn1_max, d_chunk_flags, rows, *h_epoch,
-                               narrow, d_ids, d_dists, d_counters, d_status, search_stream);
-  if (rc) return rc;
-  for (int64_t c = 1; c < nchunks; ++c) {
-    rc = upload(c);
+  // Every upload is queued before the search is launched: from pinned memory
+  // the queueing is asynchronous, so the search still starts while the
+  // chunks are in flight, and when the two streams cannot overlap (a
+  // profiler serialising work, CUDA_LAUNCH_BLOCKING) the chunks are already
+  // there instead of being queued behind a search that waits for them.
+  for (int64_t c = 0; c < nchunks; ++c) {
+    int rc = upload(c);
     if (rc) return rc;
   }
+  int rc = ggnn_query_batch_staged(X, bottom, d_top_rows, ntop, d_q_stage, m, p, d_nn1_max, d_chunk_flags, rows,
+                                   *h_epoch, narrow, d_ids, d_dists, d_counters, d_status, search_stream);
+  if (rc) return rc;
   GGNN_CUDA_TRY(cudaMemcpyAsync(h_ids, d_ids, (size_t)m * k * sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
   GGNN_CUDA_TRY(cudaMemcpyAsync(h_dists, d_dists, (size_t)m * k * sizeof(double), cudaMemcpyDeviceToHost, ss));
   GGNN_CUDA_TRY(cudaMemcpyAsync(h_counters, d_counters, (size_t)m * 5 * sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
