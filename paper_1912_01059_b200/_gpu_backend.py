@@ -55,14 +55,14 @@ def squared_l2_many(q, X, rows) -> np.ndarray:
 def _topk(dv, rows_dev, nrows, q, k):
     keep, qs = _query_dev(dv, q)
     k = int(min(k, nrows))
-    if k > 32:
-        raise NotImplementedError("exhaustive_topk on the GPU path supports k <= 32")
     t = N.torch()
     ids = N.empty((1, k), t.int32)
     dists = N.empty((1, k), t.float64)
     N.call("ggnn_exhaustive_topk", ctypes.byref(dv.struct), N.ptr(rows_dev), nrows, ctypes.byref(qs), k, N.ptr(ids),
            N.ptr(dists), N.stream_ptr())
-    return ids.cpu().numpy()[0], dists.cpu().numpy()[0]
+    ids, dists = ids.cpu().numpy()[0], dists.cpu().numpy()[0]
+    N.check_tc_timeouts("bf")
+    return ids, dists
 
 
 def exhaustive_topk(X, q, k):
@@ -96,7 +96,9 @@ def batch_bruteforce(X, member_rows, k_nn):
     dist = N.empty((m, k_nn), t.float64)
     N.call("ggnn_leaf_knn", ctypes.byref(dv.struct), N.ptr(nodes), None, N.ptr(offs), 1, m, k_nn, N.ptr(pos),
            N.ptr(dist), None, 0, None, None, None, N.stream_ptr())
-    return pos.cpu().numpy(), dist.cpu().numpy()
+    pos, dist = pos.cpu().numpy(), dist.cpu().numpy()
+    N.check_tc_timeouts("leaf")
+    return pos, dist
 
 
 def _layer_struct(adj, k_nn, sym_count, to_row_dev):
@@ -117,7 +119,9 @@ def greedy_search(X, to_row, adj, k_nn, sym_count, q, seed_ids, seed_dists, k_ou
     keep, qs = _query_dev(dv, q)
     seed_ids = np.ascontiguousarray(seed_ids, dtype=np.int32).reshape(1, -1)
     seed_dists = np.ascontiguousarray(seed_dists, dtype=np.float64).reshape(1, -1)
-    flags = N.FLAG_DISTINCT | (0 if dv.exact_integers else N.FLAG_EXACT_DISTS)
+    # exact re-score whenever keys are FP64 (float table, or float queries on a
+    # uint8 table); the kernel ignores the flag for exact uint8 / uint8 keys
+    flags = N.FLAG_DISTINCT | N.FLAG_EXACT_DISTS
     params = N.search_params(k_out, prioq_size, visited_size, tau, max_iterations, flags)
     t = N.torch()
     ids = N.empty((1, k_out), t.int32)

@@ -145,6 +145,30 @@ def call(name: str, *args) -> None:
     check(rc, name)
 
 
+# Tensor-core kernels bound their mbarrier waits (a lost MMA completion must
+# not hang the GPU) and count the timeouts in a device counter instead;
+# callers of those kernels check the counter after their results are on the
+# host, so a stalled MMA raises instead of returning garbage lists.
+_TC_SEEN: dict = {}
+
+
+def check_tc_timeouts(which: str = "both") -> None:
+    """Raise NativeError if a tensor-core kernel (leaf kNN: ggnn_tc_timeouts,
+    brute force: ggnn_bf_timeouts) timed out since the last check on this
+    device.  Reading the counters synchronises the device."""
+    names = {"leaf": ("ggnn_tc_timeouts",), "bf": ("ggnn_bf_timeouts",),
+             "both": ("ggnn_tc_timeouts", "ggnn_bf_timeouts")}[which]
+    dev = torch().cuda.current_device()
+    for name in names:
+        v = int(getattr(load(), name)())
+        if v < 0:
+            raise NativeError(f"{name}: reading the device counter failed")
+        seen = _TC_SEEN.get((name, dev), 0)
+        if v != seen:
+            _TC_SEEN[(name, dev)] = v
+            raise NativeError(f"{name}: {v - seen} tensor-core MMA wait(s) timed out; results are invalid")
+
+
 # ---------------------------------------------------------------- torch glue
 _torch = None
 

@@ -27,6 +27,7 @@ SYM_CHECK_BUDGET = 16  # expansions allowed per reachability check (build.py:31)
 SYM_CHECK_PRIOQ = 64
 SYM_CHECK_VISITED = 128
 SYM_FALLBACK = 8
+MAX_SLOTS = 32  # adjacency slots per node the kernels handle (ggnn_common.cuh MAX_K)
 # node windows per symmetrize pass: requests of x-window w are re-checked after the
 # claims of windows < w, approximating the reference's sequential x order
 # Node windows per symmetrize / merge pass: the reference walks the nodes of a
@@ -191,7 +192,9 @@ def _leaf_layer(h, j: int, nodes: np.ndarray, offsets: np.ndarray) -> int:
            max_batch, layer.k_nn, None, None, N.ptr(dev["adj"]), layer.k, N.ptr(dev["nnd"]), N.ptr(dev["dnn1"]),
            N.ptr(ws.reduced), N.stream_ptr())
     layer._version += 1
-    return int(ws.reduced.item())
+    reduced = int(ws.reduced.item())
+    N.check_tc_timeouts("leaf")
+    return reduced
 
 
 def _seg_of0(h):
@@ -216,7 +219,7 @@ def _merge_pass(h, j: int):
     dev = layer._dev
     nc = layer.node_count
     dv = DeviceVectors.of(h.dataset)
-    flags = 0 if dv.exact_integers else N.FLAG_EXACT_DISTS
+    flags = N.FLAG_EXACT_DISTS  # (a no-op for exact uint8 keys)
     params = N.search_params(cfg.k_out, cfg.prioq_size, cfg.visited_size, cfg.tau, cfg.max_iterations, flags)
     t = N.torch()
     if j == 0:
@@ -453,6 +456,9 @@ def build(dataset: Dataset, cfg: BuildConfig | None = None, threads: int = 1,
     n = dataset.n
     if n < cfg.s:
         raise ConfigError(f"dataset has {n} points but batches need at least s={cfg.s}")
+    if cfg.k > MAX_SLOTS:
+        # one warp lane per adjacency slot in every search and merge kernel
+        raise ConfigError(f"k must be <= {MAX_SLOTS} on the GPU path (got k={cfg.k})")
     rng = np.random.default_rng(cfg.seed)
     consensus_rng = np.random.default_rng((cfg.seed, 0xC0115E15))
     stats = BuildStats(threads=threads)

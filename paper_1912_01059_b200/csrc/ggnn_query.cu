@@ -248,36 +248,21 @@ __device__ __forceinline__ void set_layer(WarpSearch<TX, TQ, LP>& s, const Layer
   s.dmax = L.slack;
 }
 
-// hits -> output rows; float keys optionally re-scored sequentially
+// hits -> output rows (float keys optionally re-scored sequentially and
+// re-sorted, WarpSearch::write_out) + the five counters.  distinct_touched is
+// -1 when it was not computed (no GGNN_FLAG_DISTINCT) and when a compact
+// distinct-set overflowed (the caller reruns those queries with exact tables).
 template <typename TX, typename TQ, int LP>
-__device__ void write_hits(const WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64_t qi, const int32_t* to_row,
+__device__ void write_hits(WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64_t qi, const int32_t* to_row,
                            int extra_visited, int extra_distinct) {
-  using Key = typename VecTraits<TX, TQ>::Key;
-  const int lane = lane_id();
-  Key key;
-  int id;
-  const int nh = s.hits(key, id);
   const int k_out = a.c.k_out;
-  if (lane < k_out) {
-    double dv = __longlong_as_double(0x7ff0000000000000ll);
-    if (lane < nh) {
-      dv = KeyOps<Key>::to_d(key);
-      if constexpr (sizeof(Key) == 8) {
-        if (a.c.flags & FLAG_EXACT_DISTS) {
-          int row = to_row ? __ldg(to_row + id) : id;
-          dv = seq_sqdist<TX, TQ>(s.X + (int64_t)row * a.d, s.qs, a.d);
-        }
-      }
-    }
-    a.ids[qi * k_out + lane] = lane < nh ? id : -1;
-    a.dists[qi * k_out + lane] = dv;
-  }
-  if (lane == 0 && a.counters) {
+  s.write_out(to_row, (a.c.flags & FLAG_EXACT_DISTS) != 0, a.ids + qi * k_out, a.dists + qi * k_out);
+  if (lane_id() == 0 && a.counters) {
     int32_t* c = a.counters + qi * 5;
     c[0] = s.visited + extra_visited;
     c[1] = s.steps;
     c[2] = s.term;
-    c[3] = s.ever_overflow ? -1 : s.distinct + extra_distinct;  // -1: rerun with an exact table
+    c[3] = (a.ever == nullptr || s.ever_overflow) ? -1 : s.distinct + extra_distinct;
     c[4] = s.forgotten;
   }
 }
@@ -288,14 +273,14 @@ __device__ __forceinline__ void push_row(const SearchArgs& a, int64_t qi) {
   const int lane = lane_id();
   const int k = a.c.k_out;
   const int64_t base = (int64_t)a.push_rank * (int64_t)a.push_bb;
-  if (lane < k) {
-    const int32_t id = a.ids[qi * k + lane];
-    const double dv = a.dists[qi * k + lane];
+  for (int j = lane; j < k; j += 32) {
+    const int32_t id = a.ids[qi * k + j];
+    const double dv = a.dists[qi * k + j];
     const int32_t gid = (id >= 0 && id < a.push_gid_size) ? __ldg(a.push_gid + id) : -1;
     for (int g = 0; g < a.push_n; ++g) {
       uint8_t* blk = a.push_peers[g] + base;
-      reinterpret_cast<int32_t*>(blk)[qi * k + lane] = gid;
-      reinterpret_cast<double*>(blk + a.push_doff)[qi * k + lane] = dv;
+      reinterpret_cast<int32_t*>(blk)[qi * k + j] = gid;
+      reinterpret_cast<double*>(blk + a.push_doff)[qi * k + j] = dv;
     }
   }
   if (lane < 5 && a.counters) {
@@ -318,14 +303,24 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
   s.dmax = a.dmax;
   s.reset();
   zero_ever(s, a.ever_size);
-  // top_layer_seeds (search.py:100-112): exact top-min(k_out, ntop) over the top layer
+  // top_layer_seeds (search.py:100-112): exact top-min(k_out, ntop) over the
+  // top layer, 32 ranks per pass (one pass unless k_out and the top layer
+  // both exceed 32)
   const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
-  Key bk;
-  int bi;
-  warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, s.crow, s.ckey, bk, bi);
-  int sid = -1;
-  if (lane < kk) sid = a.top_rows ? __ldg(a.top_rows + bi) : bi;
-  s.seed(bk, sid, kk);
+  Key ak = 0;  // the previous pass's last (key, local index)
+  int ai = -1;
+  for (int b = 0; b < kk; b += 32) {
+    const int kc = min(32, kk - b);
+    Key bk;
+    int bi;
+    warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, a.top_rows, 0, (int)a.ntop, kc, s.crow, s.ckey, bk, bi, b > 0,
+                               ak, ai);
+    ak = KeyOps<Key>::shfl(bk, kc - 1);
+    ai = __shfl_sync(FULL, bi, kc - 1);
+    int sid = -1;
+    if (lane < kc) sid = a.top_rows ? __ldg(a.top_rows + bi) : bi;
+    s.seed(bk, sid, kc);
+  }
   s.run();
   // query() adds the top scan to the effort counters (search.py:134-136)
   write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
@@ -411,51 +406,91 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     hi = min(lo + a.seg_size, (int)Ls.node_count);
   }
   const int kk = min(a.c.k_out, hi - lo);
-  Key bk;
-  int bi;
-  warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, Ls.to_row, lo, hi, kk, s.crow, s.ckey, bk, bi);
-  int id = lane < kk ? bi + lo : -1;
-  int nh = kk;
   int visited = hi - lo, steps = 0, distinct = (hi - lo) - kk, forgotten = 0, term = TERM_EMPTY;
   bool ever_ovf = false;
-  for (int j = a.start - 1; j >= a.stop; --j) {
-    const LayerDev& Lj = a.layers[j];
-    const int sid = lane < nh ? __ldg(a.layers[j + 1].down + id) : -1;
-    set_layer(s, Lj);
+  if (a.c.k_out <= 32) {  // hits fit the lanes: carried between layers in registers
+    Key bk;
+    int bi;
+    warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, Ls.to_row, lo, hi, kk, s.crow, s.ckey, bk, bi);
+    int id = lane < kk ? bi + lo : -1;
+    int nh = kk;
+    for (int j = a.start - 1; j >= a.stop; --j) {
+      const LayerDev& Lj = a.layers[j];
+      const int sid = lane < nh ? __ldg(a.layers[j + 1].down + id) : -1;
+      set_layer(s, Lj);
+      s.reset();
+      zero_ever(s, a.ever_size);
+      s.seed(bk, sid, nh);
+      s.run();
+      visited += s.visited;
+      steps += s.steps;
+      distinct += s.distinct;
+      ever_ovf = ever_ovf || s.ever_overflow;
+      forgotten += s.forgotten;
+      term = s.term;
+      nh = s.hits(bk, id);
+    }
+    if (a.start == a.stop) {  // no search ran: the segment's top-kk goes into the ring for write_out
+      set_layer(s, Ls);
+      s.reset();
+      s.ever = nullptr;  // (its table is not zeroed; the count is `distinct` above)
+      s.seed(bk, id, nh);
+    }
+  } else {
+    // k_out > 32: the segment scan in passes of 32 ranks seeds the ring of
+    // the start layer; between layers the hits wait at the top of the ring
+    // (stash) while the next layer's search is seeded from them
+    set_layer(s, Ls);
     s.reset();
-    zero_ever(s, a.ever_size);
-    s.seed(bk, sid, nh);
-    s.run();
-    visited += s.visited;
-    steps += s.steps;
-    distinct += s.distinct;
-    ever_ovf = ever_ovf || s.ever_overflow;
-    forgotten += s.forgotten;
-    term = s.term;
-    nh = s.hits(bk, id);
+    uint32_t* const ever = s.ever;
+    s.ever = nullptr;  // seeding the scan's result is not a search: no distinct-set yet
+    Key ak = 0;
+    int ai = -1;
+    for (int b = 0; b < kk; b += 32) {
+      const int kc = min(32, kk - b);
+      Key bk;
+      int bi;
+      warp_topk_scan<TX, TQ, LP>(s.X, a.d, s.qs, a.lpr, Ls.to_row, lo, hi, kc, s.crow, s.ckey, bk, bi, b > 0, ak, ai);
+      ak = KeyOps<Key>::shfl(bk, kc - 1);
+      ai = __shfl_sync(FULL, bi, kc - 1);
+      s.seed(bk, lane < kc ? bi + lo : -1, kc);
+    }
+    s.ever = ever;
+    for (int j = a.start - 1; j >= a.stop; --j) {
+      const int nh = min(s.L, a.c.k_out);
+      s.stash(nh);
+      const int32_t* down = a.layers[j + 1].down;
+      set_layer(s, a.layers[j]);
+      s.reset();
+      zero_ever(s, a.ever_size);
+      for (int b = 0; b < nh; b += 32) {
+        Key sk = KeyOps<Key>::max_key();
+        int sid = -1;
+        if (b + lane < nh) {
+          s.stashed(nh, b + lane, sk, sid);
+          sid = __ldg(down + sid);
+        }
+        __syncwarp();
+        s.seed(sk, sid, min(32, nh - b));
+      }
+      s.run();
+      visited += s.visited;
+      steps += s.steps;
+      distinct += s.distinct;
+      ever_ovf = ever_ovf || s.ever_overflow;
+      forgotten += s.forgotten;
+      term = s.term;
+    }
   }
   const int k_out = a.c.k_out;
-  const int32_t* stop_rows = a.layers[a.stop].to_row;
-  if (lane < k_out) {
-    double dv = __longlong_as_double(0x7ff0000000000000ll);
-    if (lane < nh) {
-      dv = KeyOps<Key>::to_d(bk);
-      if constexpr (sizeof(Key) == 8) {
-        if (a.c.flags & FLAG_EXACT_DISTS) {
-          int row = stop_rows ? __ldg(stop_rows + id) : id;
-          dv = seq_sqdist<TX, TQ>(s.X + (int64_t)row * a.d, s.qs, a.d);
-        }
-      }
-    }
-    a.ids[qi * k_out + lane] = lane < nh ? id : -1;
-    a.dists[qi * k_out + lane] = dv;
-  }
+  s.write_out(a.layers[a.stop].to_row, (a.c.flags & FLAG_EXACT_DISTS) != 0, a.ids + qi * k_out,
+              a.dists + qi * k_out);
   if (lane == 0 && a.counters) {
     int32_t* c = a.counters + qi * 5;
     c[0] = visited;
     c[1] = steps;
     c[2] = term;
-    c[3] = ever_ovf ? -1 : distinct;
+    c[3] = (a.ever == nullptr || ever_ovf) ? -1 : distinct;
     c[4] = forgotten;
   }
 }
@@ -644,23 +679,37 @@ __global__ void __launch_bounds__(256) topk_kernel(const __grid_constant__ Searc
   Key* ckey = reinterpret_cast<Key*>(base + 128);
   TQ* qs = reinterpret_cast<TQ*>(base + 128 + align16(32 * sizeof(Key)));
   load_query<TX, TQ>(qs, a, qi);
-  const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
-  Key bk;
-  int bi;
-  warp_topk_scan<TX, TQ, LP>(reinterpret_cast<const TX*>(a.X), a.d, qs, a.lpr, a.top_rows, 0, (int)a.ntop, kk, crow,
-                         ckey, bk, bi);
+  // k_out = the requested k (any size): ranks [b, b + 32) per pass
   const int k_out = a.c.k_out;
-  if (lane < k_out) {
+  const int kk = (int)min((int64_t)k_out, a.ntop);
+  Key ak = 0;
+  int ai = -1;
+  for (int b = 0; b < k_out; b += 32) {
+    const int kc = max(0, min(32, kk - b));
     double dv = __longlong_as_double(0x7ff0000000000000ll);
-    if (lane < kk) {
-      dv = KeyOps<Key>::to_d(bk);
-      if constexpr (sizeof(Key) == 8) {
-        int row = a.top_rows ? __ldg(a.top_rows + bi) : bi;
-        dv = seq_sqdist<TX, TQ>(reinterpret_cast<const TX*>(a.X) + (int64_t)row * a.d, qs, a.d);
+    int id = INT_MAX;
+    if (kc > 0) {
+      Key bk;
+      int bi;
+      warp_topk_scan<TX, TQ, LP>(reinterpret_cast<const TX*>(a.X), a.d, qs, a.lpr, a.top_rows, 0, (int)a.ntop, kc,
+                                 crow, ckey, bk, bi, b > 0, ak, ai);
+      ak = KeyOps<Key>::shfl(bk, kc - 1);
+      ai = __shfl_sync(FULL, bi, kc - 1);
+      if (lane < kc) {
+        id = bi;
+        dv = KeyOps<Key>::to_d(bk);
+        if constexpr (sizeof(Key) == 8) {  // exact sequential FP64, then the (exact, row) order
+          int row = a.top_rows ? __ldg(a.top_rows + bi) : bi;
+          dv = seq_sqdist<TX, TQ>(reinterpret_cast<const TX*>(a.X) + (int64_t)row * a.d, qs, a.d);
+        }
       }
+      if constexpr (sizeof(Key) == 8) warp_sort(dv, id);
     }
-    a.ids[qi * k_out + lane] = lane < kk ? bi : -1;
-    a.dists[qi * k_out + lane] = dv;
+    const int o = b + lane;
+    if (o < k_out) {
+      a.ids[qi * k_out + o] = lane < kc ? id : -1;
+      a.dists[qi * k_out + o] = dv;
+    }
   }
 }
 
@@ -717,8 +766,12 @@ LayerDev to_dev(const ggnn_layer& l) {
 
 int validate_params(const ggnn_search_params* p) {
   GGNN_CHECK_ARG(p != nullptr, "null search params");
-  GGNN_CHECK_ARG(p->k_out >= 1 && p->k_out <= 32, "k_out must be in [1, 32] on the GPU path (got %d)", p->k_out);
+  GGNN_CHECK_ARG(p->k_out >= 1, "k_out must be >= 1 (got %d)", p->k_out);
   GGNN_CHECK_ARG(p->prioq_size >= 1 && p->visited_size >= 1, "cache geometry values must be >= 1");
+  // more than 32 hits are carried between passes at the top of the ring
+  // (WarpSearch::stash), which needs ring capacity k_out + prioq >= 2 * k_out
+  GGNN_CHECK_ARG(p->k_out <= 32 || p->prioq_size >= p->k_out,
+                 "k_out > 32 needs prioq_size >= k_out (got k_out=%d, prioq_size=%d)", p->k_out, p->prioq_size);
   GGNN_CHECK_ARG(p->max_iterations >= 0, "max_iterations must be >= 0");
   return GGNN_OK;
 }
@@ -900,8 +953,8 @@ int ggnn_device_info(int* sm_count, int* smem_per_block) {
 
 size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params* p, int32_t max_seeds) {
   if (!p || !(p->flags & GGNN_FLAG_DISTINCT)) return 0;
-  // max_seeds < 0: room for the exact table of every query (any seed count <= 32)
-  const uint32_t full = ever_size_for(p, max_seeds < 0 ? 32 : max_seeds, MAX_K);
+  // max_seeds < 0: room for the exact table of every query (any seed count <= max(32, k_out))
+  const uint32_t full = ever_size_for(p, max_seeds < 0 ? std::max(32, p->k_out) : max_seeds, MAX_K);
   if (max_seeds < 0) return (size_t)m * full * 4;
   return (size_t)m * std::min(full, COMPACT_EVER) * 4;
 }
@@ -1288,7 +1341,7 @@ int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const i
 int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t nrows, const ggnn_queries* Q,
                          int32_t k, int32_t* d_ids, double* d_dists, void* stream) {
   GGNN_CHECK_ARG(k >= 1, "k must be >= 1 (got %d)", k);
-  ggnn_search_params p{std::min(k, 32), 1, 1, 0, 0.0, 0};
+  ggnn_search_params p{k, k, 1, 0, 0.0, 0};
   SearchArgs a;
   int rc = fill_common(a, X, Q, &p);
   if (rc) return rc;
@@ -1296,8 +1349,7 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   // whole-table scans of uint8 data at least one X tile per split long: tensor cores
   if (bf_tc_eligible(X, d_rows, Q, k) && nrows == X->n && X->n >= 4096)
     return bf_topk_tc(X, Q, k, d_ids, d_dists, as_stream(stream));
-  GGNN_CHECK_ARG(k <= 32, "k must be <= 32 here (k <= 128 needs uint8 data with d %% 32 == 0, d <= 128, and at "
-                 "least 4096 rows); got %d", k);
+  // otherwise the warp scan, ceil(k / 32) passes over the rows
   a.top_rows = d_rows;
   a.ntop = nrows;
   a.ids = d_ids;
@@ -1322,7 +1374,7 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
 int ggnn_exhaustive_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int32_t k, int32_t* d_ids,
                             double* d_dists, void* stream) {
   GGNN_CHECK_ARG(k >= 1, "k must be >= 1 (got %d)", k);
-  ggnn_search_params p{std::min(k, 32), 1, 1, 0, 0.0, 0};
+  ggnn_search_params p{k, k, 1, 0, 0.0, 0};
   SearchArgs a;
   int rc = fill_common(a, X, Q, &p);
   if (rc) return rc;

@@ -99,6 +99,9 @@ inline int table_log2(int cap, int vsz) {
 #endif
 constexpr int PREFETCH_LINES = GGNN_PREFETCH_LINES;
 
+template <typename Key>
+__device__ void warp_sorted_out(const Key* keys, const int* ids, int n, int K, int32_t* out_ids, double* out_d);
+
 template <typename TX, typename TQ, int LP = 0>
 struct WarpSearch {
   using Key = typename VecTraits<TX, TQ>::Key;
@@ -609,6 +612,55 @@ struct WarpSearch {
     }
     return nh;
   }
+
+  // Copy the first nh ring entries to the top of the ring array, positions
+  // [cap - nh, cap), where seeding the next search (which fills [0, nh))
+  // cannot reach them while cap >= 2 * nh: hits of more than 32 entries
+  // carried from one layer's search to the next (descent).
+  __device__ void stash(int nh) {
+    const int base = c.cap - nh;
+    for (int i = lane_id(); i < nh; i += 32) {
+      if constexpr (PACK) {
+        re[base + i] = re[i];
+      } else {
+        rk[base + i] = rk[i];
+        rid[base + i] = rid[i];
+      }
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void stashed(int nh, int i, Key& key, int& id) const {
+    key = ring_key(c.cap - nh + i);
+    id = ring_id(c.cap - nh + i);
+  }
+
+  // The first min(L, k_out) ring entries -> out_ids / out_d[0, k_out), -1 /
+  // +inf padded.  With `rescore` (float keys: FP32-partial or lane-parallel
+  // sums drove the search) each hit's distance is recomputed with the
+  // reference's sequential FP64 _sqdist and the hits are re-sorted by
+  // (exact distance, id), the order the reference's ring would hold them in.
+  // to_row_map: layer id -> dataset row (nullptr = identity).
+  __device__ void write_out(const int32_t* to_row_map, bool rescore, int32_t* out_ids, double* out_d) {
+    const int lane = lane_id();
+    const int nh = min(L, c.k_out);
+    if constexpr (!PACK) {
+      if (rescore) {
+        for (int i = lane; i < nh; i += 32) {
+          const int id = rid[i];
+          const int row = to_row_map ? __ldg(to_row_map + id) : id;
+          rk[i] = seq_sqdist<TX, TQ>(X + (int64_t)row * d, qs, d);
+        }
+        __syncwarp();
+        warp_sorted_out<Key>(rk, rid, nh, c.k_out, out_ids, out_d);
+        return;
+      }
+    }
+    for (int i = lane; i < c.k_out; i += 32) {
+      const bool ok = i < nh;
+      out_ids[i] = ok ? ring_id(i) : -1;
+      out_d[i] = ok ? KO::to_d(ring_key(i)) : __longlong_as_double(0x7ff0000000000000ll);
+    }
+  }
 };
 
 // Merge one unsorted chunk (ck, cx) (one pair per lane, invalid lanes hold
@@ -646,10 +698,13 @@ __device__ __forceinline__ void topk_merge_chunk(Key& bk, int& bi, Key ck, int c
 // Exhaustive top-kk (kk <= 32) over rows[lo..hi) (or the index range itself
 // when rows is null), ties by local index; the result sits in lanes [0, kk)
 // as (key, local index) -- the reference's exhaustive_topk (_core.pyx:86-104).
+// With `after`, only pairs ordered strictly after (ak, ai) compete: pass p of
+// a top-K with K > 32 selects ranks [32p, 32p + 32) this way.
 template <typename TX, typename TQ, int LP = 0>
 __device__ void warp_topk_scan(const TX* X, int64_t d, const TQ* qs, int lpr, const int32_t* rows, int lo, int hi,
                                int kk, int* crow, typename VecTraits<TX, TQ>::Key* ckey,
-                               typename VecTraits<TX, TQ>::Key& bk, int& bi) {
+                               typename VecTraits<TX, TQ>::Key& bk, int& bi, bool after = false,
+                               typename VecTraits<TX, TQ>::Key ak = 0, int ai = -1) {
   using Key = typename VecTraits<TX, TQ>::Key;
   using KO = KeyOps<Key>;
   const int lane = lane_id();
@@ -666,10 +721,55 @@ __device__ void warp_topk_scan(const TX* X, int64_t d, const TQ* qs, int lpr, co
     if (lane < cnt) {
       ck = ckey[lane];
       cx = base + lane - lo;
+      if (after && !key_less(ak, ai, ck, cx)) {
+        ck = KO::max_key();
+        cx = INT_MAX;
+      }
     }
     __syncwarp();
     topk_merge_chunk(bk, bi, ck, cx, kk);
   }
+}
+
+// Top-K (any K) of n (key, id) pairs held in shared memory (keys[i], ids[i],
+// distinct ids), written ascending by (key, id) to out_ids / out_d[0, K):
+// ceil(K / 32) passes of the warp top-32, pass p keeping the pairs after the
+// last one pass p - 1 emitted.  Positions >= n are padded (-1, +inf).
+template <typename Key>
+__device__ void warp_sorted_out(const Key* keys, const int* ids, int n, int K, int32_t* out_ids, double* out_d) {
+  using KO = KeyOps<Key>;
+  const int lane = lane_id();
+  Key ak = 0;
+  int ai = -1;
+  for (int b = 0; b < K; b += 32) {
+    Key bk = KO::max_key();
+    int bi = INT_MAX;
+    if (b < n) {
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        Key ck = KO::max_key();
+        int cx = INT_MAX;
+        if (i < n) {
+          ck = keys[i];
+          cx = ids[i];
+          if (b > 0 && !key_less(ak, ai, ck, cx)) {
+            ck = KO::max_key();
+            cx = INT_MAX;
+          }
+        }
+        topk_merge_chunk(bk, bi, ck, cx, 32);
+      }
+      ak = KO::shfl(bk, 31);
+      ai = __shfl_sync(FULL, bi, 31);
+    }
+    const int o = b + lane;
+    if (o < K) {
+      const bool ok = o < n;
+      out_ids[o] = ok ? bi : -1;
+      out_d[o] = ok ? KO::to_d(bk) : __longlong_as_double(0x7ff0000000000000ll);
+    }
+  }
+  __syncwarp();
 }
 
 }  // namespace ggnn

@@ -5,9 +5,8 @@
 // through the warp 32 at a time and folded into a running ascending top-32
 // by the bitonic merge of search.cuh (topk_merge_chunk), keyed by
 // (distance f64, dataset id) -- the reference's sort key (shard.py:106).
-// The per-shard lists are already ascending, so the first entry of the list
-// that supplies the overall best hit identifies its shard (ids of different
-// shards are disjoint), which gives terminated_by (shard.py:108).
+// The shard whose list holds the overall best hit (ids of different shards
+// are disjoint) gives terminated_by (shard.py:108).
 #include <climits>
 #include "ggnn_capi_util.cuh"
 #include "ggnn_p2p.h"
@@ -77,24 +76,46 @@ __global__ void __launch_bounds__(256) shard_merge_kernel(const __grid_constant_
   if (q >= a.m) return;
   const int lane = lane_id();
   using KO = KeyOps<double>;
-  double bk = KO::max_key();
-  int bi = INT_MAX;
   const int total = a.G * a.k_in;
   long long vsum = 0, tsum = 0;
-  for (int base = 0; base < total; base += 32) {
-    const int e = base + lane;
-    double ck = KO::max_key();
-    int cx = INT_MAX;
-    if (e < total) {
-      const int g = e / a.k_in, j = e - g * a.k_in;
-      const uint8_t* blk = a.blocks + (size_t)g * a.block_bytes;
-      const int32_t id = reinterpret_cast<const int32_t*>(blk)[q * a.k_in + j];
-      if (id >= 0) {
-        ck = reinterpret_cast<const double*>(blk + a.dists_off)[q * a.k_in + j];
-        cx = id;
+  // ranks [b, b + 32) of the merged list per pass: pass b keeps the pairs
+  // ordered after the last one of pass b - 32 (one pass for k_out <= 32)
+  int best = INT_MAX;
+  double ak = 0.0;
+  int ai = -1;
+  for (int b = 0; b < a.k_out; b += 32) {
+    const int kk = min(32, a.k_out - b);
+    double bk = KO::max_key();
+    int bi = INT_MAX;
+    if (b == 0 || ai != INT_MAX) {
+      for (int base = 0; base < total; base += 32) {
+        const int e = base + lane;
+        double ck = KO::max_key();
+        int cx = INT_MAX;
+        if (e < total) {
+          const int g = e / a.k_in, j = e - g * a.k_in;
+          const uint8_t* blk = a.blocks + (size_t)g * a.block_bytes;
+          const int32_t id = reinterpret_cast<const int32_t*>(blk)[q * a.k_in + j];
+          if (id >= 0) {
+            ck = reinterpret_cast<const double*>(blk + a.dists_off)[q * a.k_in + j];
+            cx = id;
+            if (b > 0 && !key_less(ak, ai, ck, cx)) {
+              ck = KO::max_key();
+              cx = INT_MAX;
+            }
+          }
+        }
+        topk_merge_chunk(bk, bi, ck, cx, kk);
       }
     }
-    topk_merge_chunk(bk, bi, ck, cx, a.k_out);
+    if (b == 0) best = __shfl_sync(FULL, bi, 0);
+    ak = KO::shfl(bk, 31);
+    ai = __shfl_sync(FULL, bi, 31);
+    if (lane < kk) {
+      const bool ok = bi != INT_MAX;
+      a.out_ids[q * a.k_out + b + lane] = ok ? bi : -1;
+      a.out_dists[q * a.k_out + b + lane] = ok ? bk : KO::max_key();
+    }
   }
   if (a.out_cnt) {
     for (int g = lane; g < a.G; g += 32) {
@@ -108,23 +129,23 @@ __global__ void __launch_bounds__(256) shard_merge_kernel(const __grid_constant_
       tsum += __shfl_xor_sync(FULL, tsum, o);
     }
   }
-  const int best = __shfl_sync(FULL, bi, 0);
-  if (lane < a.k_out) {
-    const bool ok = bi != INT_MAX;
-    a.out_ids[q * a.k_out + lane] = ok ? bi : -1;
-    a.out_dists[q * a.k_out + lane] = ok ? bk : KO::max_key();
-  }
   if (a.out_cnt) {
     int term = TERM_EMPTY;  // shard.py:108 "queue-empty" when nothing was found
     if (best != INT_MAX) {
-      // exactly one shard list starts with `best` (shard ids are disjoint)
+      // exactly one shard list holds `best` (shard ids are disjoint).  It is
+      // not necessarily that list's first entry: a shard orders its hits by
+      // (dist, LOCAL id), and a permutation can reverse two tied hits, so
+      // every entry is searched, not position 0 alone.
       int src = -1;
-      for (int g0 = 0; g0 < a.G && src < 0; g0 += 32) {
-        const int g = g0 + lane;
+      for (int base = 0; base < total && src < 0; base += 32) {
+        const int e = base + lane;
         bool hit = false;
-        if (g < a.G) hit = reinterpret_cast<const int32_t*>(a.blocks + (size_t)g * a.block_bytes)[q * a.k_in] == best;
+        if (e < total) {
+          const int g = e / a.k_in, j = e - g * a.k_in;
+          hit = reinterpret_cast<const int32_t*>(a.blocks + (size_t)g * a.block_bytes)[q * a.k_in + j] == best;
+        }
         const unsigned bal = __ballot_sync(FULL, hit);
-        if (bal) src = g0 + __ffs(bal) - 1;
+        if (bal) src = (base + __ffs(bal) - 1) / a.k_in;
       }
       if (src >= 0)
         term = reinterpret_cast<const int32_t*>(a.blocks + (size_t)src * a.block_bytes + a.cnt_off)[q * 5 + 2];
@@ -259,7 +280,7 @@ static int shard_merge_impl(const void* d_blocks, int32_t G, int64_t m, int32_t 
                             uint32_t epoch, int32_t* error, void* stream) {
   GGNN_CHECK_ARG(G >= 1 && m >= 0 && k_in >= 1, "ggnn_shard_merge: bad shape G=%d m=%lld k_in=%d", G, (long long)m,
                  k_in);
-  GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32, "ggnn_shard_merge: k_out must be in [1, 32], got %d", k_out);
+  GGNN_CHECK_ARG(k_out >= 1, "ggnn_shard_merge: k_out must be >= 1, got %d", k_out);
   if (m == 0) return GGNN_OK;
   GGNN_CHECK_ARG(d_blocks && d_out_ids && d_out_dists, "ggnn_shard_merge: null pointer");
   MergeShardArgs a;

@@ -20,8 +20,13 @@ from . import _native as N
 
 _ARRAY_CACHE: dict = {}
 
-# hierarchies up to this many adjacency bytes are content-hashed on every call
-_HASH_LIMIT = 64 << 20
+# Host-resident hierarchies up to this many adjacency bytes are content-hashed
+# on every device_hierarchy() call, so the reference's tests that write layer
+# arrays in place (SURVEY 8b "host-object coherence") see their writes without
+# a touch(); the hash costs well under a millisecond at this size.  Larger
+# hierarchies are re-uploaded only on a version bump: after writing their
+# numpy arrays directly call layer.touch() or Hierarchy.invalidate_caches().
+_HASH_LIMIT = 1 << 20
 
 
 class DeviceVectors:

@@ -119,6 +119,7 @@ class ShardGroup:
         ids_p, dists_p, _ = block_pointers(send, 0, m, k)
         N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), ids_p,
                dists_p, N.stream_ptr())
+        N.check_tc_timeouts("bf")
         N.call("ggnn_shard_globalize", ids_p, m * k, N.ptr(self.gid_dev()), int(self.gid_host.shape[0]),
                N.stream_ptr())
         self.exchange(send, recv)

@@ -8,6 +8,7 @@ distances are squared L2; tau is applied in squared space (search.py:45-54).
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -50,7 +51,9 @@ def stopping_check(d_next: float, d_best_k: float, d_best_1: float, d_nn1_max: f
 @dataclass
 class BatchResult:
     """Array form of a query batch: ids / dists (m, k_out), -1 / inf padded;
-    counters (m, 5) = visited, steps, term code, distinct, forgotten."""
+    counters (m, 5) = visited, steps, term code, distinct, forgotten.
+    distinct_touched is -1 when the batch did not compute it (query_arrays
+    without distinct=True); batch_query / query always compute it."""
 
     ids: np.ndarray
     dists: np.ndarray
@@ -71,8 +74,11 @@ def _params(cfg: QueryConfig, flags: int):
 
 
 def _flags(dv: DeviceVectors, distinct: bool) -> int:
-    f = 0 if dv.exact_integers else N.FLAG_EXACT_DISTS
-    return f | (N.FLAG_DISTINCT if distinct else 0)
+    """FLAG_EXACT_DISTS always: whenever a search's keys are FP64 (a float
+    table, or float queries on a uint8 table) the returned hits are re-scored
+    with the reference's sequential _sqdist and re-sorted; the kernel ignores
+    the flag for uint8 queries on a uint8 table, whose keys are exact."""
+    return N.FLAG_EXACT_DISTS | (N.FLAG_DISTINCT if distinct else 0)
 
 
 def _qflags(dh, distinct: bool) -> int:
@@ -198,7 +204,18 @@ def _query_host_staged(dh, Q: np.ndarray, cfg: QueryConfig):
     return BatchResult(ids_h.numpy(), dists_h.numpy(), cnt_h.numpy())
 
 
+# The staging buffers and stream pair of a device are shared by every call on
+# that device: host threads calling query_arrays concurrently take turns
+# (their searches would share the GPU anyway).
+_HOST_LOCK = threading.Lock()
+
+
 def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
+    with _HOST_LOCK:
+        return _query_host_fast_locked(dh, Q, cfg)
+
+
+def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     t = N.torch()
     # staged: uint8 tables only (float32 rows stay float and their upload is
     # 4x larger; measured slower than the chunked path on gist1m)
@@ -450,7 +467,9 @@ def exact_knn_rows(dataset, rows: np.ndarray, k: int):
     dists = N.empty((len(rows), k), t.float64)
     N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), N.ptr(ids),
            N.ptr(dists), N.stream_ptr())
-    return ids.cpu().numpy(), dists.cpu().numpy()
+    ids, dists = ids.cpu().numpy(), dists.cpu().numpy()
+    N.check_tc_timeouts("bf")
+    return ids, dists
 
 
 def exact_knn(dataset, queries: np.ndarray, k: int):
@@ -465,4 +484,6 @@ def exact_knn(dataset, queries: np.ndarray, k: int):
     dists = N.empty((m, k), t.float64)
     N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), N.ptr(ids),
            N.ptr(dists), N.stream_ptr())
-    return ids.cpu().numpy(), dists.cpu().numpy()
+    ids, dists = ids.cpu().numpy(), dists.cpu().numpy()
+    N.check_tc_timeouts("bf")
+    return ids, dists

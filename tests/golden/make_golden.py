@@ -34,6 +34,9 @@ Fixtures:
                     rows L2-normalised) at 100k x 96 + 1000 held-out queries:
                     query() ids of the reference-built graph at tau 0.3 / 0.6
                     / 1.0 / 2.0 (medium-scale build parity on clustered data).
+  latent200k.npz    the C2 generator (latent16) at 200k x 128 + 5000 fresh
+                    queries: query() ids of the reference-built graph at tau
+                    0.3 / 0.45 / 0.6 (build parity closer to C2's scale).
   sharded_int.npz   reference build_sharded of the kernels_int data
                     (shard_size 250 -> 3 shards), every shard's graph, the
                     permutation, and query_sharded results (ids, dists,
@@ -245,6 +248,24 @@ def make_latent20k(R):
     print("latent20k build", stats.build_seconds, "s")
 
 
+def make_latent200k(R):
+    """C2's generator at 200k x 128 (latent16, integer-valued) with 5000 fresh
+    queries: the reference-built graph's query() ids at tau 0.3 / 0.45 / 0.6
+    (build parity one order of magnitude closer to C2 than latent20k)."""
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, queries = make_latent16(n=200_000, d=128, m=5000, seed=1234)
+    sha = hashlib.sha256(base.tobytes() + queries.tobytes()).hexdigest()
+    h, stats = R.build(R.Dataset(base.copy()), R.BuildConfig(seed=7))
+    out = {"data_sha256": np.array(sha), "build_seconds_ref": np.float64(stats.build_seconds)}
+    for tau in (0.3, 0.45, 0.6):
+        ids, dists, cnt = query_table(R, h, queries, R.QueryConfig(k_out=10, tau=tau))
+        t = f"{int(round(tau * 100)):03d}"
+        out[f"q{t}_ids"], out[f"q{t}_cnt"] = ids, cnt[:, :3]
+    np.savez_compressed(OUT / "latent200k.npz", **out)
+    print("latent200k build", stats.build_seconds, "s")
+
+
 def deep_c4(n, m, d=96, seed=1234):
     """C4 generator at size n (1024 clusters as in bench.py --workload deep10m)."""
     from paper_1912_01059_b200.data import gen_synthetic
@@ -288,6 +309,8 @@ def main():
         make_latent20k(R)
     if "deep100k" in which:
         make_deep100k(R)
+    if "latent200k" in which:
+        make_latent200k(R)
 
 
 if __name__ == "__main__":

@@ -153,6 +153,11 @@ def test_query_arrays_matches_batch_query(golden_sift):
     np.testing.assert_array_equal(arr.ids, g["q6_ids"])
     np.testing.assert_array_equal(arr.dists, g["q6_dists"])
     np.testing.assert_array_equal(arr.counters[:, [0, 1, 2, 4]], g["q6_cnt"][:, [0, 1, 2, 4]])
+    # distinct_touched is not computed on this path: -1, never a wrong count
+    assert (arr.counters[:, 3] == -1).all()
+    assert all(r.distinct_touched == -1 for r in arr.results()[:5])
+    dev = ga.query_arrays(h, Q, cfg, out="device")
+    assert (dev[2][:, 3].cpu().numpy() == -1).all()
 
 
 def test_hierarchical_query_matches_checker(golden_int):
@@ -191,20 +196,27 @@ def test_query_arrays_integral_and_fractional_queries(golden_sift):
     np.testing.assert_array_equal(a.ids, g["q6_ids"])
     np.testing.assert_array_equal(a.dists, g["q6_dists"])
     np.testing.assert_array_equal(a.counters[:, :3], g["q6_cnt"][:, :3])
-    Qf = (queries + 0.25).astype(np.float32)
-    b = ga.query_arrays(h, Qf, cfg)
+    # random fractional queries: every key is an FP64 sum whose rounding
+    # depends on the summation order, so the returned hits must be re-scored
+    # sequentially (and re-sorted) to equal the reference's _sqdist values
+    rng = np.random.default_rng(17)
+    Qf = (queries + rng.uniform(-3.0, 3.0, size=queries.shape)).astype(np.float32)
     layers = [(L.adjacency, L.k_nn, L.sym_count) for L in h.layers]
     X = h.dataset.vectors
-    same = 0
-    for i in range(len(Qf)):
-        ids, dd, v, t, term, _, _ = O.query(layers, h.to_bottom, X, Qf[i], 10, 0.6, h.stats.d_nn1_max)
-        for node, dist in zip(b.ids[i], b.dists[i]):
-            if node >= 0:
-                assert O.squared_l2(Qf[i], X[node]) == dist
-        if np.array_equal(b.ids[i, :len(ids)], ids):
-            same += 1
-            np.testing.assert_array_equal(b.dists[i, :len(dd)], dd)
-    assert same >= 0.98 * len(Qf)
+    for b in (ga.query_arrays(h, Qf, cfg), ga.query_arrays(h, Qf, cfg, out="device"), None):
+        if b is None:  # batch_query (with distinct_touched and forgotten)
+            res = ga.batch_query(h, Qf, cfg)
+        elif isinstance(b, tuple):
+            res = ga.search.BatchResult(*(t.cpu().numpy() for t in b)).results()
+        else:
+            res = b.results()
+        for i, r in enumerate(res):
+            ids, dd, v, t, term, dist, fg = O.query(layers, h.to_bottom, X, Qf[i], 10, 0.6, h.stats.d_nn1_max)
+            np.testing.assert_array_equal(r.ids, ids)
+            np.testing.assert_array_equal(r.dists, dd)
+            assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.forgotten) == (v, t, term, fg)
+            if b is None:
+                assert r.distinct_touched == dist
 
 
 def test_staged_host_path_equals_chunked(golden_sift):
@@ -333,3 +345,86 @@ def test_distinct_touched_exact_past_compact_table(golden_sift):
             v, t, term, distinct, forgotten)
         big += int(distinct > 3072)
     assert big > 0  # the overflow path was exercised
+
+
+@pytest.mark.parametrize("k_out", [33, 50, 100])
+def test_k_out_above_32_vs_checker(k_out):
+    """k_out > 32 (the reference accepts any k_out >= 1, config.py:66-75):
+    hits are written and re-sorted in passes of 32; every query equals the
+    CPU checker bit for bit (ids, dists and all five counters), on an integer
+    table and on a float table (re-scored hits)."""
+    h, rng = _random_int_hierarchy(5, n=2500)
+    Q = rng.integers(0, 256, size=(120, h.dim)).astype(np.float32)
+    cfg = ga.QueryConfig(k_out=k_out, tau=0.8, prioq_size=2 * k_out + 7, visited_size=300)
+    for Qx in (Q, (Q + rng.uniform(-0.5, 0.5, size=Q.shape)).astype(np.float32)):
+        got = ga.batch_query(h, Qx, cfg)
+        arr = ga.query_arrays(h, Qx, cfg)
+        for i, (q, r) in enumerate(zip(Qx, got)):
+            want = O.query(oracle_layers(h), h.to_bottom, h.vectors(), q, cfg.k_out, cfg.tau, h.stats.d_nn1_max,
+                           cfg.max_iterations, cfg.prioq_size, cfg.visited_size)
+            np.testing.assert_array_equal(r.ids, want[0])
+            np.testing.assert_array_equal(r.dists, want[1])
+            assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched,
+                    r.forgotten) == tuple(want[2:])
+            np.testing.assert_array_equal(arr.ids[i, :len(want[0])], want[0])
+            assert (arr.ids[i, len(want[0]):] == -1).all()
+
+
+@pytest.mark.parametrize("k_out", [40, 100])
+def test_k_out_above_32_single_layer_top_scan(k_out):
+    """A one-layer hierarchy (n < s * g) seeds from an exhaustive scan of
+    all n points: top-min(k_out, n) > 32 is selected in passes of 32 ranks
+    (ties by position, like exhaustive_topk); hierarchical_query's descent
+    and the float brute force take the same multi-pass path."""
+    rng = np.random.default_rng(k_out)
+    X = rng.integers(0, 6, size=(110, 8)).astype(np.float32)  # many distance ties
+    ds = ga.Dataset(X)
+    h, _ = ga.build(ds, ga.BuildConfig(seed=3))
+    assert h.num_layers == 1
+    Q = rng.integers(0, 6, size=(60, 8)).astype(np.float32)
+    cfg = ga.QueryConfig(k_out=k_out, tau=0.6, prioq_size=2 * k_out)
+    for q, r in zip(Q, ga.batch_query(h, Q, cfg)):
+        want = O.query(oracle_layers(h), h.to_bottom, X, q, k_out, 0.6, h.stats.d_nn1_max, 1000, 2 * k_out, 512)
+        np.testing.assert_array_equal(r.ids, want[0])
+        np.testing.assert_array_equal(r.dists, want[1])
+        assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched,
+                r.forgotten) == tuple(want[2:])
+        hq = ga.hierarchical_query(h, q, cfg)  # start == stop: the exhaustive top-k of the layer
+        ids, dd = O.exhaustive_topk(X, q, min(k_out, len(X)))
+        np.testing.assert_array_equal(hq.ids, ids)
+        np.testing.assert_array_equal(hq.dists, dd)
+    Xf = rng.standard_normal((3000, 16)).astype(np.float32)
+    Qf = rng.standard_normal((40, 16)).astype(np.float32)
+    gt = ga.brute_force_oracle(ga.Dataset(Xf), Qf, k_out)
+    for i in range(len(Qf)):
+        ids, dd = O.exhaustive_topk(Xf, Qf[i], k_out)
+        np.testing.assert_array_equal(gt.ids[i], ids)
+        np.testing.assert_array_equal(gt.dists[i], dd)
+
+
+def test_k_out_above_32_descent_vs_checker(golden_sift):
+    """hierarchical_query with k_out = 40 on the reference's sift10k graph:
+    the 40 hits of each layer seed the next layer's search (carried at the
+    top of the ring), equal to the checker composition of search.py:140-210."""
+    g, h, queries = golden_sift
+    cfg = ga.QueryConfig(k_out=40, tau=0.5, prioq_size=96)
+    X = h.vectors()
+    top = h.num_layers - 1
+    for q in queries[:25]:
+        r = ga.hierarchical_query(h, q, cfg)
+        rows = h.rows_for(top)
+        local, dists = O.exhaustive_topk(X[rows], q, min(cfg.k_out, len(rows)))
+        ids = local.astype(np.int32)
+        v, t, dist_cnt, fg, term = len(rows), 0, len(rows) - len(ids), 0, 1
+        for j in range(top - 1, -1, -1):
+            seeds = h.local_ids(j, h.rows_for(j + 1)[ids])
+            L = h.layers[j]
+            bound = h.stats.d_nn1_max if j == 0 else L.live_d_nn1_max()
+            ids, dists, nv, nt, term, nd, nf = O.greedy_search(X, h.rows_for(j), L.adjacency, L.k_nn, L.sym_count,
+                                                               q, seeds, dists, cfg.k_out, cfg.tau, bound,
+                                                               cfg.max_iterations, cfg.prioq_size, cfg.visited_size)
+            v, t, dist_cnt, fg = v + nv, t + nt, dist_cnt + nd, fg + nf
+        np.testing.assert_array_equal(r.ids, ids)
+        np.testing.assert_array_equal(r.dists, dists)
+        assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten) == (
+            v, t, term, dist_cnt, fg)

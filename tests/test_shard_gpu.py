@@ -30,7 +30,8 @@ def test_same_graph_sharded_query_bitwise():
     np.testing.assert_array_equal(one.ids, g["q_ids"][3][g["q_ids"][3] >= 0])
 
 
-@pytest.mark.parametrize("G,k_in,k_out", [(1, 10, 10), (3, 6, 6), (8, 10, 10), (5, 24, 24), (9, 12, 7), (40, 4, 32)])
+@pytest.mark.parametrize("G,k_in,k_out", [(1, 10, 10), (3, 6, 6), (8, 10, 10), (5, 24, 24), (9, 12, 7), (40, 4, 32),
+                                          (3, 50, 40), (4, 40, 100), (8, 100, 100)])
 def test_merge_kernel_vs_oracle(G, k_in, k_out):
     rng = np.random.default_rng(G * 100 + k_in)
     m = 257
@@ -67,6 +68,55 @@ def test_merge_kernel_vs_oracle(G, k_in, k_out):
         np.testing.assert_array_equal(dists[i, :nh], gd)
         assert (ids[i, nh:] == -1).all() and np.isinf(dists[i, nh:]).all()
         assert tuple(cnt[i]) == (v, t, term, 0, 0)
+
+
+@pytest.mark.parametrize("G,k_in,k_out", [(2, 10, 10), (3, 6, 4), (8, 10, 10), (33, 3, 5)])
+def test_merge_kernel_local_order_ties(G, k_in, k_out):
+    """Blocks as the sharded search really writes them: each shard's list is
+    ordered by (dist, LOCAL id) and then globalized through a permutation that
+    reverses local order, so inside a shard two hits tied on distance come out
+    in descending global id.  The merged ids, dists, sums and terminated_by
+    (taken from the shard holding the best hit, which need not be its list's
+    first entry) equal the reference's _merge_shard_results (shard.py:91-110)."""
+    rng = np.random.default_rng(G * 31 + k_in)
+    m, per = 300, 400
+    n_total = G * per
+    perm = np.arange(n_total, dtype=np.int32)[::-1].copy()  # reverses every tie
+    bb, doff, coff = block_layout(m, k_in)
+    raw = np.zeros(G * bb, dtype=np.uint8)
+    parts_all = [[] for _ in range(m)]
+    for gi in range(G):
+        off = gi * per
+        blk = raw[gi * bb:(gi + 1) * bb]
+        ids = blk[: m * k_in * 4].view(np.int32).reshape(m, k_in)
+        ds = blk[doff: doff + m * k_in * 8].view(np.float64).reshape(m, k_in)
+        cnt = blk[coff: coff + m * 20].view(np.int32).reshape(m, 5)
+        for i in range(m):
+            nh = int(rng.integers(0, k_in + 1)) if i % 11 == 0 else k_in
+            d = rng.integers(0, 3, size=nh).astype(np.float64)  # almost every hit ties
+            loc = rng.choice(per, size=nh, replace=False).astype(np.int32)
+            order = np.lexsort((loc, d))  # the shard's own (dist, local id) order
+            loc, d = loc[order], d[order]
+            ids[i] = -1
+            ds[i] = np.inf
+            ids[i, :nh] = perm[off + loc]  # ggnn_shard_globalize
+            ds[i, :nh] = d
+            cnt[i] = [int(rng.integers(0, 999)), int(rng.integers(0, 99)), gi % 3, 5, 5]
+            parts_all[i].append((off, loc, d, cnt[i, 0], cnt[i, 1], cnt[i, 2]))
+    ids, dists, cnt = merge_blocks(N.to_dev(raw), G, m, k_in, k_out)
+    ids, dists, cnt = ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy()
+    wrong_first = 0
+    for i in range(m):
+        gi_, gd, v, t, term = O.merge_shard_results(parts_all[i], perm, k_out)
+        nh = len(gi_)
+        np.testing.assert_array_equal(ids[i, :nh], gi_)
+        np.testing.assert_array_equal(dists[i, :nh], gd)
+        assert (ids[i, nh:] == -1).all()
+        assert tuple(cnt[i]) == (v, t, term, 0, 0), i
+        if nh:
+            heads = {int(perm[p[0] + p[1][0]]) for p in parts_all[i] if len(p[1])}
+            wrong_first += int(gi_[0]) not in heads
+    assert wrong_first > 0  # the case position-0 matching missed is exercised
 
 
 def test_gpu_built_shards_merge_exact_and_persist(tmp_path):
@@ -306,5 +356,9 @@ def test_bruteforce_tensor_cores_large_k(k):
         ri, rd = O.exhaustive_topk(X, Q[i], k)
         np.testing.assert_array_equal(gt.ids[i], ri)
         np.testing.assert_array_equal(gt.dists[i], rd)
-    with pytest.raises(ValueError):
-        ga.brute_force_oracle(ga.Dataset(X[:1000]), Q, 40)  # below the tensor-core size: k <= 32 only
+    # below the tensor-core size the warp scan selects ceil(k / 32) passes of 32
+    small = ga.brute_force_oracle(ga.Dataset(X[:1000]), Q, k)
+    for i in range(0, m, 9):
+        ri, rd = O.exhaustive_topk(X[:1000], Q[i], k)
+        np.testing.assert_array_equal(small.ids[i], ri)
+        np.testing.assert_array_equal(small.dists[i], rd)
