@@ -38,6 +38,15 @@ int ggnn_leaf_knn_tc(const ggnn_vectors *X, const int32_t *d_nodes, const int32_
  * library was loaded (0 in a healthy run; synchronizes). */
 int ggnn_tc_timeouts(void);
 
+/* Build accounting: while d_acc != NULL, every search launched
+ * from this host thread by ggnn_merge_descent, ggnn_descent_batch,
+ * ggnn_greedy_batch and the sym-check entry points adds its visited count to
+ * d_acc[0] and its steps to d_acc[1] (device uint64, caller-zeroed), so the
+ * algorithmic bytes of a phase are d_acc[0] * d * e + d_acc[1] * (4k + 4).
+ * NULL switches it off (the default; the query kernel is never counted).
+ * No reference counterpart (the reference reports no such totals). */
+int ggnn_search_accounting(unsigned long long *d_acc);
+
 /* Replaces: the per-node hierarchical_query calls of merge_layer
  * (build.py:146-197, search.py:140-210) for all m nodes of layer `stop` at
  * once.  Query i is base row d_query_rows[i]; it brute-forces the segment

@@ -164,6 +164,32 @@ class BuildStats:
     dropped_sym_links: int = 0
     build_seconds: float = 0.0
     threads: int = 1
+    # build accounting (build(..., accounting=True)): per phase, the searches'
+    # visited / steps totals (ggnn_search_accounting) and the leaf kNN's
+    # multiply-adds (sum over batches of m_b^2 * d)
+    search_visited: dict[str, int] = field(default_factory=dict)
+    search_steps: dict[str, int] = field(default_factory=dict)
+    leaf_macs: int = 0
+
+    def accounting_summary(self, d: int, e: int, k: int = 24) -> dict | None:
+        """Algorithmic bytes per phase, V * d * e + T * (4k + 4) summed over
+        the phase's searches (SURVEY.md 8d "Build accounting"), and the
+        bytes / second each phase reached."""
+        if not self.search_visited:
+            return None
+        per = {}
+        for key, v in self.search_visited.items():
+            b = v * d * e + self.search_steps.get(key, 0) * (4 * k + 4)
+            sec = self.phase_seconds.get(key, 0.0)
+            per[key] = {"bytes": b, "GB_per_s": b / sec / 1e9 if sec > 0 else None}
+        total = sum(p["bytes"] for p in per.values())
+        t_search = sum(self.phase_seconds.get(key, 0.0) for key in per)
+        top = dict(sorted(per.items(), key=lambda kv: -kv[1]["bytes"])[:6])
+        return {"search_bytes_total": total, "search_seconds": t_search,
+                "search_GB_per_s": total / t_search / 1e9 if t_search else None,
+                "visited_total": int(sum(self.search_visited.values())),
+                "steps_total": int(sum(self.search_steps.values())),
+                "leaf_knn_flops": 2 * self.leaf_macs, "top_phases": top}
 
 
 def _merge_query_config(cfg: BuildConfig) -> QueryConfig:
@@ -449,9 +475,10 @@ def _select_level(h: Hierarchy, level: int, rng: np.random.Generator) -> np.ndar
 
 
 def build(dataset: Dataset, cfg: BuildConfig | None = None, threads: int = 1,
-          track_consensus: bool = False) -> tuple[Hierarchy, BuildStats]:
+          track_consensus: bool = False, accounting: bool = False) -> tuple[Hierarchy, BuildStats]:
     """Construct the full hierarchy on the GPU (build.py:297-406).
-    Deterministic for a fixed (dataset, cfg.seed); `threads` is ignored."""
+    Deterministic for a fixed (dataset, cfg.seed); `threads` is ignored.
+    accounting=True fills BuildStats' per-phase search totals."""
     cfg = cfg or BuildConfig()
     n = dataset.n
     if n < cfg.s:
@@ -480,12 +507,49 @@ def build(dataset: Dataset, cfg: BuildConfig | None = None, threads: int = 1,
     if track_consensus:
         sample = consensus_rng.choice(n, size=min(CONSENSUS_SAMPLE, n), replace=False)
 
+    acc = None
+    if accounting:
+        acc = N.torch().zeros(2, dtype=N.torch().int64, device=N.device())
+        N.call("ggnn_search_accounting", N.ptr(acc))
+
     def timed(key, fn, *args):
         t0 = time.perf_counter()
         out = fn(*args)
         _sync()
         stats.phase_seconds[key] = stats.phase_seconds.get(key, 0.0) + time.perf_counter() - t0
+        if acc is not None:
+            v, t = (int(x) for x in acc.tolist())
+            if v or t:
+                stats.search_visited[key] = stats.search_visited.get(key, 0) + v
+                stats.search_steps[key] = stats.search_steps.get(key, 0) + t
+                acc.zero_()
         return out
+
+    try:
+        _build_levels(h, cfg, stats, timed, perm, offsets, l, rng, sample)
+    finally:
+        if acc is not None:
+            N.call("ggnn_search_accounting", None)
+    if accounting:
+        sizes = np.diff(np.asarray(offsets, dtype=np.int64))
+        stats.leaf_macs = int((sizes * sizes).sum()) * dataset.d
+        for L in h.layers[1:]:
+            stats.leaf_macs += (L.node_count // cfg.s) * cfg.s * cfg.s * dataset.d
+    h.stats = compute_stats(h)
+    per_layer = [float(L._dev["symc"].double().mean().item()) for L in h.layers]
+    stats.sym_used_per_layer = per_layer
+    stats.mean_sym_used = per_layer[0]
+    _sync()
+    stats.build_seconds = time.perf_counter() - t_begin
+    from .device import _token
+
+    h._device_cache = (_token(h), G.device_hierarchy_from_build(h))
+    return h, stats
+
+
+def _build_levels(h, cfg, stats, timed, perm, offsets, l, rng, sample):
+    """The level loop of build(): leaf kNN + symmetrize of layer 0, then per
+    level selection, coarse brute force, merges and refinements."""
 
     def refine(j):
         return _symmetrize_dev(h, j, cfg.tau_build, _merge_pass(h, j))
@@ -518,14 +582,3 @@ def build(dataset: Dataset, cfg: BuildConfig | None = None, threads: int = 1,
                 if j == 0 and sample is not None:
                     stats.consensus_trajectory.append((f"level{level}/refine{r}", _sample_consensus(h, sample)))
         stats.d_nn1_trajectory.append(_bottom_d_nn1(h))
-
-    h.stats = compute_stats(h)
-    per_layer = [float(L._dev["symc"].double().mean().item()) for L in h.layers]
-    stats.sym_used_per_layer = per_layer
-    stats.mean_sym_used = per_layer[0]
-    _sync()
-    stats.build_seconds = time.perf_counter() - t_begin
-    from .device import _token
-
-    h._device_cache = (_token(h), G.device_hierarchy_from_build(h))
-    return h, stats

@@ -24,6 +24,15 @@ int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_i
                cudaStream_t st);
 
 static thread_local std::string g_err;
+// ggnn_search_accounting: (visited, steps) totals of the build-type searches
+static thread_local unsigned long long* g_acc = nullptr;
+
+__device__ __forceinline__ void account(unsigned long long* acc, long long visited, long long steps) {
+  if (acc && lane_id() == 0) {
+    atomicAdd(acc, (unsigned long long)visited);
+    atomicAdd(acc + 1, (unsigned long long)steps);
+  }
+}
 void set_error(const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -141,6 +150,7 @@ struct SearchArgs {
   uint32_t qepoch;
   int qconv;
   int32_t* qstatus;
+  unsigned long long* acc;  // build accounting (visited, steps) or nullptr
 };
 
 // Persistent warps: with a work counter (zeroed before the launch) every warp
@@ -371,6 +381,7 @@ __device__ __forceinline__ void greedy_kernel_one(const SearchArgs& a, uint8_t* 
     s.seed(sk, sid, cnt);
   }
   s.run();
+  account(a.acc, s.visited, s.steps);
   write_hits(s, a, qi, a.layer.to_row, 0, 0);
 }
 
@@ -482,6 +493,7 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
       term = s.term;
     }
   }
+  account(a.acc, visited, steps);
   const int k_out = a.c.k_out;
   s.write_out(a.layers[a.stop].to_row, (a.c.flags & FLAG_EXACT_DISTS) != 0, a.ids + qi * k_out,
               a.dists + qi * k_out);
@@ -547,6 +559,7 @@ struct SymArgs {
   int32_t* stage;
   int32_t x_end;  // recheck only requests of nodes x < x_end
   int* work;      // persistent-warp item counter (nullptr: one item per warp)
+  unsigned long long* acc;  // build accounting (visited, steps) or nullptr
 };
 
 template <typename TX, int LP>
@@ -612,6 +625,7 @@ __device__ __forceinline__ void symcheck_kernel_one(const SymArgs& a, uint8_t* s
     s.reset();
     s.seed(KeyOps<Key>::from_d(dxz), lane == 0 ? z : -1, 1);
     s.run();
+    account(a.acc, s.visited, s.steps);
     v = s.term ? 1 : 2;
     // fallbacks: closest explored ids excluding x and z (_core.pyx:420-426)
     const int nh = min(s.L, a.c.k_out);
@@ -886,6 +900,7 @@ int fill_common(SearchArgs& a, const ggnn_vectors* X, const ggnn_queries* Q, con
   int rc = validate_params(p);
   if (rc) return rc;
   memset(&a, 0, sizeof(a));
+  a.acc = g_acc;
   a.X = X->d_data;
   a.n = X->n;
   a.d = X->d;
@@ -942,6 +957,11 @@ int attach_ever(SearchArgs& a, const ggnn_search_params* p, int32_t max_seeds, i
 extern "C" {
 
 const char* ggnn_last_error(void) { return g_err.c_str(); }
+
+int ggnn_search_accounting(unsigned long long* d_acc) {
+  g_acc = d_acc;
+  return GGNN_OK;
+}
 int ggnn_version(void) { return 100; }
 
 int ggnn_device_info(int* sm_count, int* smem_per_block) {
@@ -1254,6 +1274,7 @@ int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const d
   if (npairs <= 0) return GGNN_OK;
   SymArgs a;
   memset(&a, 0, sizeof(a));
+  a.acc = g_acc;
   a.X = X->d_data;
   a.d = X->d;
   a.lpr = choose_lpr(X->d, X->dtype, X->dtype, reinterpret_cast<uintptr_t>(X->d_data));
@@ -1287,6 +1308,7 @@ int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_
   if (nreq <= 0) return GGNN_OK;
   SymArgs a;
   memset(&a, 0, sizeof(a));
+  a.acc = g_acc;
   a.X = X->d_data;
   a.d = X->d;
   a.lpr = choose_lpr(X->d, X->dtype, X->dtype, reinterpret_cast<uintptr_t>(X->d_data));
@@ -1317,6 +1339,7 @@ int ggnn_sym_check_batch(const ggnn_vectors* X, const ggnn_layer* layer, const i
   if (npairs <= 0) return GGNN_OK;
   SymArgs a;
   memset(&a, 0, sizeof(a));
+  a.acc = g_acc;
   a.X = X->d_data;
   a.d = X->d;
   a.lpr = choose_lpr(X->d, X->dtype, X->dtype, reinterpret_cast<uintptr_t>(X->d_data));

@@ -1,4 +1,4 @@
-"""One shard per GPU: multi-process sharded build and search.
+"""Shards over GPUs: multi-process sharded build and search.
 
 The paper's multi-GPU mode (reference shard.py:1-12,
 91-128): shard r of the seeded permutation lives on rank r (one process per
@@ -27,18 +27,37 @@ from .search import BatchResult
 
 
 class ShardGroup:
-    """This rank's shard plus the process group that holds the others."""
+    """This rank's shards plus the process group that holds the others.
 
-    def __init__(self, h, gid_of_local: np.ndarray, group=None):
+    Global shard i lives on rank i // S (S = shards per rank, the same on
+    every rank), so an all-gather of every rank's S consecutive blocks lays
+    the blocks out in global shard order.  `ShardGroup(h, gid)` is the
+    one-shard-per-rank case; without an initialised process group the group
+    is this process alone (world 1: one GPU searching all its shards in turn,
+    the north star's QPS_1)."""
+
+    def __init__(self, h=None, gid_of_local: np.ndarray | None = None, group=None, shards=None):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-        self.h = h
-        self.gid_host = np.ascontiguousarray(gid_of_local, dtype=np.int32)
-        self._gid_dev = None
+        self.on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.world = dist.get_world_size(group) if self.on else 1
+        if shards is None:
+            shards = [(h, gid_of_local)]
+        self.shards = [(hh, np.ascontiguousarray(g, dtype=np.int32)) for hh, g in shards]
+        self.h, self.gid_host = self.shards[0]
+        self._gid_devs = {}
+
+    @property
+    def per_rank(self) -> int:
+        return len(self.shards)
+
+    @property
+    def n_blocks(self) -> int:
+        """Shards in the whole group (= merged blocks per query)."""
+        return self.world * self.per_rank
 
     # ---------------------------------------------------------- construction
     @classmethod
@@ -65,11 +84,37 @@ class ShardGroup:
         grp.build_stats = stats
         return grp
 
+    @classmethod
+    def from_local_shards(cls, loader, n_shards: int, cfg: BuildConfig | None = None, group=None, build_fn=None):
+        """Rank-local construction: this rank builds only its own shards
+        i = rank * S ... rank * S + S - 1 (S = n_shards / world) from
+        `loader(i) -> (Dataset, gid)` (gid: the shard's dataset ids, int32);
+        no rank ever holds the whole dataset (C5: 8 x 12.5M uint8 shards)."""
+        import torch.distributed as dist
+
+        from .build import build
+
+        cfg = cfg or BuildConfig()
+        on = dist.is_available() and dist.is_initialized()
+        world, rank = (dist.get_world_size(group), dist.get_rank(group)) if on else (1, 0)
+        if n_shards % world:
+            raise ValueError(f"{n_shards} shards do not divide over {world} ranks")
+        per = n_shards // world
+        shards, stats = [], []
+        for i in range(rank * per, (rank + 1) * per):
+            ds, gid = loader(i)
+            h, st = (build_fn or build)(ds, cfg)
+            shards.append((h, gid))
+            stats.append(st)
+        grp = cls(group=group, shards=shards)
+        grp.build_stats = stats
+        return grp
+
     # -------------------------------------------------------------- search
-    def gid_dev(self):
-        if self._gid_dev is None:
-            self._gid_dev = N.to_dev(self.gid_host)
-        return self._gid_dev
+    def gid_dev(self, s: int = 0):
+        if s not in self._gid_devs:
+            self._gid_devs[s] = N.to_dev(self.shards[s][1])
+        return self._gid_devs[s]
 
     def block_bytes(self, m: int, k: int) -> int:
         from .shard import block_layout
@@ -80,20 +125,29 @@ class ShardGroup:
         return N.empty((nbytes,), N.torch().uint8)
 
     def search_block(self, Q: np.ndarray, cfg: QueryConfig, buf) -> None:
-        """Search the local shard into block 0 of `buf`, ids globalized."""
+        """Search every local shard s into block s of `buf`, ids globalized
+        (the shards one after the other on this rank's stream)."""
+        for s, (h, gid) in enumerate(self.shards):
+            self.search_shard(s, h, gid, Q, cfg, buf)
+
+    def search_shard(self, s: int, h, gid, Q: np.ndarray, cfg: QueryConfig, buf) -> None:
         from .shard import search_into_block
 
-        search_into_block(self.h, Q, cfg, buf, 0, self.gid_dev())
+        search_into_block(h, Q, cfg, buf, s, self.gid_dev(s))
 
     def merge(self, recv, m: int, cfg: QueryConfig):
         from .shard import merge_blocks
 
-        return merge_blocks(recv, self.world, m, cfg.k_out, cfg.k_out)
+        return merge_blocks(recv, self.n_blocks, m, cfg.k_out, cfg.k_out)
 
     def exchange(self, send, recv) -> None:
         """All-gather of the shard blocks (NCCL on device buffers; a gloo
         group -- CPU tests, several ranks sharing one GPU -- stages through
-        host memory)."""
+        host memory; world 1: the blocks are already all here)."""
+        if not self.on:
+            if recv.data_ptr() != send.data_ptr():
+                recv.copy_(send)
+            return
         if recv.is_cuda and self.dist.get_backend(self.group) == "gloo":
             r = recv.cpu()
             self.dist.all_gather_into_tensor(r, send.cpu(), group=self.group)
@@ -102,8 +156,8 @@ class ShardGroup:
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
 
     def exact_arrays(self, queries: np.ndarray, k: int, out: str = "numpy"):
-        """Exact global top-k (k <= 32) of a replicated batch: every rank
-        scans its shard (ggnn_exhaustive_topk) into its block, then the same
+        """Exact global top-k of a replicated batch: every rank scans its
+        shards (ggnn_exhaustive_topk) into its blocks, then the same
         all-gather + merge as a search (ground truth for sharded recall)."""
         from .device import DeviceVectors
         from .shard import block_pointers
@@ -111,22 +165,22 @@ class ShardGroup:
         Q = np.ascontiguousarray(queries, dtype=np.float32)
         m = Q.shape[0]
         bb = self.block_bytes(m, k)
-        send = self.new_buffer(bb)
+        send = self.new_buffer(self.per_rank * bb)
         send.zero_()
-        recv = self.new_buffer(self.world * bb)
-        dv = DeviceVectors.of(self.h.dataset)
-        dq, qs = dv.queries(Q)
-        ids_p, dists_p, _ = block_pointers(send, 0, m, k)
-        N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), ids_p,
-               dists_p, N.stream_ptr())
-        N.check_tc_timeouts("bf")
-        N.call("ggnn_shard_globalize", ids_p, m * k, N.ptr(self.gid_dev()), int(self.gid_host.shape[0]),
-               N.stream_ptr())
+        recv = self.new_buffer(self.n_blocks * bb) if self.on else send
+        for s, (h, gid) in enumerate(self.shards):
+            dv = DeviceVectors.of(h.dataset)
+            dq, qs = dv.queries(Q)
+            ids_p, dists_p, _ = block_pointers(send, s, m, k)
+            N.call("ggnn_exhaustive_topk", N.ctypes.byref(dv.struct), None, dv.n, N.ctypes.byref(qs), int(k), ids_p,
+                   dists_p, N.stream_ptr())
+            N.check_tc_timeouts("bf")
+            N.call("ggnn_shard_globalize", ids_p, m * k, N.ptr(self.gid_dev(s)), int(gid.shape[0]), N.stream_ptr())
+            del dq
         self.exchange(send, recv)
         from .shard import merge_blocks
 
-        ids, dists, cnt = merge_blocks(recv, self.world, m, k, k)
-        del dq
+        ids, dists, cnt = merge_blocks(recv, self.n_blocks, m, k, k)
         if out == "device":
             return ids, dists
         return np.asarray(ids.cpu()), np.asarray(dists.cpu())
@@ -142,11 +196,13 @@ class ShardGroup:
             Q = Q[None, :]
         m = Q.shape[0]
         if exchange == "p2p":
+            if self.per_rank != 1 or not self.on:
+                raise ValueError("the fused exchange needs exactly one shard per rank in a process group")
             ids, dists, cnt = self.p2p(m, cfg.k_out).query(Q, cfg)
         elif exchange == "nccl":
             bb = self.block_bytes(m, cfg.k_out)
-            send = self.new_buffer(bb)
-            recv = self.new_buffer(self.world * bb)
+            send = self.new_buffer(self.per_rank * bb)
+            recv = self.new_buffer(self.n_blocks * bb) if self.on else send
             self.search_block(Q, cfg, send)
             self.exchange(send, recv)
             ids, dists, cnt = self.merge(recv, m, cfg)

@@ -79,3 +79,38 @@ def make_latent16_shard(n=1_000_000, d=128, shard=0, seed=1234, as_float=False):
         hi = min(n, lo + CHUNK)
         out[lo:hi] = _latent_draw(np.random.default_rng((seed, 0x5AD, shard, c)), A, C, hi - lo, d, as_float)
     return out
+
+
+def make_latent16_queries(m=10000, d=128, batch=1, seed=1234, as_float=False):
+    """Query batch `batch` >= 1 of the latent16 workload: m further rows of the
+    same distribution (the shared (A, C) of `seed`) from the stream
+    (seed, 0x9E57, batch).  Batch 0 is the query set make_latent16 returns
+    (bench.py: a fresh batch every step)."""
+    rng0 = np.random.default_rng(seed)
+    A = rng0.standard_normal((16, d)) / 4.0
+    C = rng0.standard_normal((64, 16)) * 2.0
+    return _latent_draw(np.random.default_rng((seed, 0x9E57, batch)), A, C, m, d, as_float)
+
+
+def make_deep_like(n, m, d=96, seed=1234, clusters=1024):
+    """C4 (Deep10M-shaped): the reference's clustered generator (data.py:163-192,
+    `clusters` Gaussian centres) with rows L2-normalised; base = the first n
+    rows, queries = the m rows held out after them."""
+    from .data import gen_synthetic
+
+    X = gen_synthetic(n + m, d, seed=seed, law="clustered", clusters=clusters).vectors.astype(np.float64)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    X = X.astype(np.float32)
+    return X[:n].copy(), X[n:].copy()
+
+
+def make_deep_like_queries(m, d=96, batch=1, seed=1234, clusters=1024):
+    """Query batch `batch` >= 1 of the C4 workload: rows around the same
+    cluster centres (the generator's first draw from `seed`), drawn from the
+    stream (seed, 0xDEE9, batch), L2-normalised."""
+    centers = np.random.default_rng(seed).standard_normal((clusters, d)) * 5.0
+    rng = np.random.default_rng((seed, 0xDEE9, batch))
+    X = centers[rng.integers(0, clusters, size=m)] + rng.standard_normal((m, d)) * 0.25
+    X = X.astype(np.float32).astype(np.float64)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    return X.astype(np.float32)

@@ -34,34 +34,35 @@ class CpuShardGroup(ShardGroup):
     def new_buffer(self, nbytes):
         return torch.zeros(nbytes, dtype=torch.uint8)
 
-    def search_block(self, Q, cfg, buf):
+    def search_shard(self, s, h, gid, Q, cfg, buf):
         m, k = Q.shape[0], cfg.k_out
         bb, doff, coff = block_layout(m, k)
-        raw = buf.numpy()
+        raw = buf.numpy()[s * bb:(s + 1) * bb]
         ids = raw[: m * k * 4].view(np.int32).reshape(m, k)
         dists = raw[doff: doff + m * k * 8].view(np.float64).reshape(m, k)
         cnt = raw[coff: coff + m * 20].view(np.int32).reshape(m, 5)
-        X = self.h.vectors
+        X = h.vectors
+        g = self.rank * self.per_rank + s  # global shard index
         for i in range(m):
             lid, ld = O.exhaustive_topk(X, Q[i], k)
             ids[i] = -1
             dists[i] = np.inf
-            ids[i, : len(lid)] = self.gid_host[lid]
+            ids[i, : len(lid)] = gid[lid]
             dists[i, : len(lid)] = ld
-            cnt[i] = [X.shape[0], 1 + self.rank, self.rank % 3, 7, 9]
+            cnt[i] = [X.shape[0], 1 + g, g % 3, 7, 9]
 
     def merge(self, recv, m, cfg):
         k = cfg.k_out
         bb, doff, coff = block_layout(m, k)
         raw = recv.numpy()
-        n_total = int(max(raw[g * bb: g * bb + m * k * 4].view(np.int32).max() for g in range(self.world))) + 1
+        n_total = int(max(raw[g * bb: g * bb + m * k * 4].view(np.int32).max() for g in range(self.n_blocks))) + 1
         ident = np.arange(n_total, dtype=np.int32)
         out_ids = np.full((m, k), -1, dtype=np.int32)
         out_d = np.full((m, k), np.inf)
         out_c = np.zeros((m, 5), dtype=np.int32)
         for i in range(m):
             parts = []
-            for g in range(self.world):
+            for g in range(self.n_blocks):
                 blk = raw[g * bb:(g + 1) * bb]
                 ids = blk[: m * k * 4].view(np.int32).reshape(m, k)[i]
                 ds = blk[doff: doff + m * k * 8].view(np.float64).reshape(m, k)[i]
@@ -131,3 +132,66 @@ def test_sharded_query_plumbing_gloo(world):
             assert rc[i, 1] == sum(1 + g for g in range(world))
             assert rc[i, 2] == owner[ids[0]] % 3
             assert rc[i, 3] == 0 and rc[i, 4] == 0
+
+
+N_SHARDS = 8
+
+
+def _shard_loader(i):
+    """Rank-local loader of shard i of the 8-shard layout (the seeded
+    permutation cut into 8 contiguous slices, shard.py:54-65)."""
+    X, _ = _data()
+    perm = np.random.default_rng(11).permutation(X.shape[0]).astype(np.int32)
+    size = -(-X.shape[0] // N_SHARDS)
+    gid = perm[i * size:(i + 1) * size]
+    return ga.Dataset(X[gid].copy()), gid
+
+
+def _local_worker(rank, world, port, q):
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X, Q = _data()
+        grp = CpuShardGroup.from_local_shards(_shard_loader, N_SHARDS, build_fn=lambda sub, c: (sub, None))
+        res = grp.query_arrays(Q, ga.QueryConfig(k_out=K_OUT, prioq_size=16))
+        q.put((rank, res.ids, res.dists, res.counters, [g for _, g in grp.shards]))
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_eight_shards_over_ranks_equal_one_rank(world):
+    """A fixed 8-shard index over 2 and 4 ranks (each rank loads and holds
+    only its 8 / world shards) answers exactly like one process holding all
+    8 shards and searching them in turn (the north star's QPS_1 layout);
+    both equal the global brute force."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    runs = {}
+    for w in (1, world):
+        procs = [ctx.Process(target=_local_worker, args=(r, w, port + (w > 1), q)) for r in range(w)]
+        for p in procs:
+            p.start()
+        runs[w] = sorted([q.get(timeout=120) for _ in range(w)], key=lambda t: t[0])
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    X, Q = _data()
+    one = runs[1][0]
+    assert len(one[4]) == N_SHARDS
+    held = [g for r in runs[world] for g in r[4]]  # ranks hold consecutive shards in global order
+    assert len(held) == N_SHARDS and all(len(r[4]) == N_SHARDS // world for r in runs[world])
+    for a, b in zip(held, one[4]):
+        np.testing.assert_array_equal(a, b)
+    for r, ids, ds, cnt, _ in runs[world]:
+        np.testing.assert_array_equal(ids, one[1])
+        np.testing.assert_array_equal(ds, one[2])
+        np.testing.assert_array_equal(cnt, one[3])
+    for i in range(Q.shape[0]):
+        ids, ds = O.exhaustive_topk(X, Q[i], K_OUT)
+        np.testing.assert_array_equal(one[1][i], ids)
+        np.testing.assert_array_equal(one[2][i], ds)
+        assert one[3][i, 1] == sum(1 + g for g in range(N_SHARDS))
