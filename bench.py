@@ -78,8 +78,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ggnn", choices=["ggnn", "reference"])
     ap.add_argument("--workload", default="sift1m", choices=sorted(WORKLOADS))
-    ap.add_argument("--n", type=int, default=None, help="override the workload's point count")
-    ap.add_argument("--d", type=int, default=None)
+    ap.add_argument("--points", dest="n", type=int, default=None, help="override the workload's point count")
+    ap.add_argument("--dim", dest="d", type=int, default=None, help="override the workload's dimension")
     ap.add_argument("--queries", type=int, default=None, help="queries per step (default: the workload's)")
     ap.add_argument("--batches", type=int, default=8, help="distinct query batches cycled over the steps")
     ap.add_argument("--gt-queries", type=int, default=None, help="ground-truth subsample (default: all of batch 0 "
@@ -907,7 +907,7 @@ def run_reference(args):
     root = Path(tempfile.mkdtemp(prefix="ggnn_ref_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None))
     try:
         cmd = [sys.executable, str(ROOT / "bench.py"), "--prep-reference", str(root), "--workload", args.workload,
-               "--n", str(args.n), "--d", str(args.d), "--queries", str(args.queries)]
+               "--points", str(args.n), "--dim", str(args.d), "--queries", str(args.queries)]
         if args.tau is not None:
             cmd += ["--tau", str(args.tau)]
         if args.gt_queries is not None:

@@ -275,6 +275,228 @@ bool leaf_tc_eligible(const ggnn_vectors* X, int64_t max_batch) {
          (reinterpret_cast<uintptr_t>(X->d_data) & 15) == 0;
 }
 
+// ----------------------------------------------- leaf kNN on tcgen05 (f32)
+// Float rows: the Gram matrix of the batch on the tensor cores as 3xTF32
+// (x = hi + lo, x.y ~ hi.hi + hi.lo + lo.hi; tcgen05.mma kind::tf32, F32
+// accumulators in TMEM), the rows centred on the batch mean first so the
+// products stay on the scale of the distances.  That gives each pair an
+// APPROXIMATE distance a_ij = n_i + n_j - 2 g_ij with a rigorous error bound
+// |a_ij - r_ij| <= beta_i (r_ij = the reference's sequential FP64 _sqdist):
+//   beta_i = (8 K 2^-23 + 2^-18) (|x_i'| + max_j |x_j'|)^2
+// (fp32 accumulation of 3K tf32 products, the split's dropped lo.lo term,
+// the centring's rounding and the FP64 norms, each over-estimated 2x).  Row i
+// keeps every j with a_ij <= A_k + 2 beta_i, A_k its k-th smallest a_ij: any
+// other j has r_ij > A_k + beta_i >= r of k candidates, so the exact top-k_nn
+// (r, position) is among the candidates.  Thread i then re-scores its
+// candidates with the sequential FP64 sum and selects by (r, position) --
+// batch_bruteforce (_core.pyx:107-130) bit for bit.  A row with more than
+// TF_CAND candidates (a pathological batch) re-scores every j instead.
+constexpr int TF_KC = 64;     // tf32 elements per staged K chunk
+constexpr int TF_CAND = 48;   // candidate slots per row
+
+inline size_t leaf_tf32_smem(int64_t d, int k_nn) {
+  return 2 * (size_t)TC_ROWS * TF_KC * 4      // hi / lo chunk, interleaved K-major
+         + (((size_t)d * 4 + 15) & ~size_t(15))  // batch mean
+         + (size_t)TC_ROWS * 8                 // FP64 norms of the centred rows
+         + (size_t)TC_ROWS * TF_CAND * 4       // candidate positions
+         + (size_t)TC_ROWS * k_nn * 12         // per-row sorted lists (FP64 key + position)
+         + 64;                                 // mbarrier, TMEM address, max norm
+}
+
+__global__ void __launch_bounds__(128, 1) leaf_knn_tf32_kernel(const __grid_constant__ LeafArgs a, int64_t nbatches) {
+  extern __shared__ __align__(16) uint8_t smem_tf[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = (int)a.d;
+  const int k_nn = a.k_nn;
+  float* Hi = reinterpret_cast<float*>(smem_tf);
+  float* Lo = Hi + TC_ROWS * TF_KC;
+  float* mean = Lo + TC_ROWS * TF_KC;
+  double* nrm = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(mean) + (((size_t)d * 4 + 15) & ~size_t(15)));
+  int32_t* cand = reinterpret_cast<int32_t*>(nrm + TC_ROWS);
+  double* lk = reinterpret_cast<double*>(cand + TC_ROWS * TF_CAND);
+  int32_t* lp = reinterpret_cast<int32_t*>(lk + TC_ROWS * k_nn);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(lp + TC_ROWS * k_nn) + 15) & ~uintptr_t(15));
+  uint32_t* taddr = reinterpret_cast<uint32_t*>(mbar + 1);
+  double* nmax = reinterpret_cast<double*>(mbar + 2);
+  if (warp == 0) tc::tmem_alloc<128>(taddr);
+  if (tid == 0) tc::mbar_init(mbar, 1);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *taddr;
+  const float* X = reinterpret_cast<const float*>(a.X);
+  double* mk = lk + tid * k_nn;
+  int32_t* mp = lp + tid * k_nn;
+  int32_t* mc = cand + tid * TF_CAND;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t sbo = (uint32_t)(TF_KC * 4 / 16) * 128u;
+  uint32_t phase = 0;
+  for (int64_t b = blockIdx.x; b < nbatches; b += gridDim.x) {
+    const int64_t off = a.offsets[b];
+    const int m = (int)(a.offsets[b + 1] - off);
+    const int n_pad = max(16, (m + 15) & ~15);
+    const int32_t my_row = tid < m ? (a.rows ? a.rows[off + tid] : a.nodes[off + tid]) : 0;
+    const float* xi = X + (int64_t)my_row * d;
+    // batch mean (fp32; any centre works -- the bound uses the centred norms)
+    for (int e = tid; e < d; e += blockDim.x) {
+      float acc = 0.0f;
+      for (int r = 0; r < m; ++r) {
+        const int32_t row = a.rows ? a.rows[off + r] : a.nodes[off + r];
+        acc += __ldg(X + (int64_t)row * d + e);
+      }
+      mean[e] = acc / (float)m;
+    }
+    __syncthreads();
+    double ni = 0.0;
+    for (int k0 = 0; k0 < d; k0 += TF_KC) {
+      const int kc = min(TF_KC, d - k0);  // a multiple of 8 (eligibility)
+      // thread tid stages its row's chunk: centred, split into tf32 hi / lo
+      for (int e = 0; e < TF_KC; e += 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tid < m && e < kc) {
+          v = __ldg(reinterpret_cast<const float4*>(xi + k0 + e));
+          v.x -= mean[k0 + e];
+          v.y -= mean[k0 + e + 1];
+          v.z -= mean[k0 + e + 2];
+          v.w -= mean[k0 + e + 3];
+          ni += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+        }
+        float4 h, l;
+        h.x = tc::to_tf32(v.x);
+        h.y = tc::to_tf32(v.y);
+        h.z = tc::to_tf32(v.z);
+        h.w = tc::to_tf32(v.w);
+        l.x = tc::to_tf32(v.x - h.x);
+        l.y = tc::to_tf32(v.y - h.y);
+        l.z = tc::to_tf32(v.z - h.z);
+        l.w = tc::to_tf32(v.w - h.w);
+        const uint32_t o = tc::il_offset(tid, e * 4, TF_KC * 4);
+        *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Hi) + o) = h;
+        *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Lo) + o) = l;
+      }
+      tc::fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t idesc = tc::idesc_tf32(TC_ROWS, n_pad);
+        const uint32_t hb = tc::smem_u32(Hi), lb = tc::smem_u32(Lo);
+        for (int s = 0; s < (kc >> 3); ++s) {
+          const uint64_t dh = tc::smem_desc(hb + (uint32_t)s * 256u, 128u, sbo);
+          const uint64_t dl = tc::smem_desc(lb + (uint32_t)s * 256u, 128u, sbo);
+          tc::mma_tf32(tmem, dh, dh, idesc, (k0 > 0 || s > 0) ? 1u : 0u);
+          tc::mma_tf32(tmem, dh, dl, idesc, 1u);
+          tc::mma_tf32(tmem, dl, dh, idesc, 1u);
+        }
+        tc::commit(mbar);
+      }
+      __syncwarp();
+      const bool ok = tc::mbar_wait(mbar, phase);
+      phase ^= 1u;
+      tc::fence_after_sync();
+      if (!ok && lane == 0) atomicAdd(&g_tc_timeouts, 1);
+      __syncthreads();  // the chunk buffers are free again
+    }
+    nrm[tid] = tid < m ? ni : 0.0;
+    if (tid == 0) *nmax = 0.0;
+    __syncthreads();
+    if (tid < m) atomicMax(reinterpret_cast<unsigned long long*>(nmax), (unsigned long long)__double_as_longlong(ni));
+    __syncthreads();
+    const int k_eff = min(k_nn, m - 1);
+    if (k_eff < k_nn && tid == 0 && a.reduced) atomicAdd(a.reduced, 1);
+    const double bnd = (8.0 * d * 0x1p-23 + 0x1p-18) * (sqrt(ni) + sqrt(*nmax)) * (sqrt(ni) + sqrt(*nmax));
+    // pass 1: the k_eff smallest approximate distances of row tid
+    for (int j = 0; j < k_eff; ++j) mk[j] = KeyOps<double>::max_key();
+    for (int c0 = 0; c0 < n_pad; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + lane_base + (uint32_t)c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = c0 + j;
+        if (tid < m && col < m && col != tid && k_eff > 0) {
+          const double ap = ni + nrm[col] - 2.0 * (double)__uint_as_float(v[j]);
+          if (ap < mk[k_eff - 1]) {
+            int p = k_eff - 1;
+            while (p > 0 && mk[p - 1] > ap) {
+              mk[p] = mk[p - 1];
+              --p;
+            }
+            mk[p] = ap;
+          }
+        }
+      }
+    }
+    // pass 2: candidates a_ij <= A_k + 2 beta
+    const double lim = k_eff > 0 ? mk[k_eff - 1] + 2.0 * bnd : -1.0;
+    int nc = 0;
+    for (int c0 = 0; c0 < n_pad; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + lane_base + (uint32_t)c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = c0 + j;
+        if (tid < m && col < m && col != tid && k_eff > 0) {
+          const double ap = ni + nrm[col] - 2.0 * (double)__uint_as_float(v[j]);
+          if (ap <= lim) {
+            if (nc < TF_CAND) mc[nc] = col;
+            ++nc;
+          }
+        }
+      }
+    }
+    // exact re-score (the reference's sequential FP64 _sqdist) and selection
+    // by (distance, position)
+    if (tid < m && k_eff > 0) {
+      for (int j = 0; j < k_eff; ++j) {
+        mk[j] = KeyOps<double>::max_key();
+        mp[j] = INT_MAX;
+      }
+      const bool all = nc > TF_CAND;
+      const int cnt = all ? m : nc;
+      for (int t = 0; t < cnt; ++t) {
+        const int col = all ? t : mc[t];
+        if (col == tid) continue;
+        const int32_t rj = a.rows ? a.rows[off + col] : a.nodes[off + col];
+        const double r = LeafRowAccess<float>::dist(xi, X + (int64_t)rj * d, d);
+        if (key_less(r, col, mk[k_eff - 1], mp[k_eff - 1])) {
+          int p = k_eff - 1;
+          while (p > 0 && key_less(r, col, mk[p - 1], mp[p - 1])) {
+            mk[p] = mk[p - 1];
+            mp[p] = mp[p - 1];
+            --p;
+          }
+          mk[p] = r;
+          mp[p] = col;
+        }
+      }
+    }
+    if (tid < m) {
+      const int64_t gi = off + tid;
+      const int32_t node = a.nodes[gi];
+      for (int j = 0; j < k_nn; ++j) {
+        const bool v = j < k_eff;
+        const int pos = v ? mp[j] : -1;
+        const double dd = v ? mk[j] : KeyOps<double>::max_key();
+        if (a.pos) a.pos[gi * k_nn + j] = pos;
+        if (a.dist) a.dist[gi * k_nn + j] = dd;
+        if (a.adj && v) {
+          a.adj[(int64_t)node * a.k + j] = a.nodes[off + pos];
+          a.nnd[(int64_t)node * k_nn + j] = dd;
+        }
+      }
+      if (a.dnn1) a.dnn1[node] = k_eff > 0 ? mk[0] : KeyOps<double>::max_key();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
+  if (warp == 0) tc::tmem_free<128>(tmem);
+}
+
+bool leaf_tf32_eligible(const ggnn_vectors* X, int64_t max_batch, int k_nn) {
+  return X->dtype == GGNN_F32 && max_batch >= 2 && max_batch <= TC_ROWS && X->d % 8 == 0 &&
+         (reinterpret_cast<uintptr_t>(X->d_data) & 15) == 0 && leaf_tf32_smem(X->d, k_nn) <= 200 * 1024;
+}
+
 // ------------------------------------------------------------- merge rows
 // One warp per node x: direct slots := the k_nn smallest (dist, id) of the
 // current direct list united with the descent hits (x itself and ids already
@@ -574,8 +796,18 @@ static int leaf_knn_impl(const ggnn_vectors* X, const int32_t* d_nodes, const in
     GGNN_LAUNCH_CHECK();
     return GGNN_OK;
   }
-  GGNN_CHECK_ARG(!force_tc, "the tensor-core leaf kNN needs uint8 rows with d %% 32 == 0, d <= 512, batches <= %d",
-                 TC_ROWS);
+  if (leaf_tf32_eligible(X, max_batch, k_nn)) {
+    const size_t smem = leaf_tf32_smem(X->d, k_nn);
+    DevInfo di = dev_info();
+    const int per_sm = std::max(1, std::min((int)(((size_t)228 * 1024) / (smem + 1024)), 4));
+    const int64_t grid = std::min<int64_t>(nbatches, (int64_t)std::max(di.sm_count, 1) * per_sm);
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    leaf_knn_tf32_kernel<<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+    GGNN_LAUNCH_CHECK();
+    return GGNN_OK;
+  }
+  GGNN_CHECK_ARG(!force_tc, "the tensor-core leaf kNN needs uint8 rows with d %% 32 == 0, d <= 512, or float rows "
+                 "with d %% 8 == 0, and batches of 2..%d rows", TC_ROWS);
   const size_t esz = X->dtype == GGNN_U8 ? 1 : 4;
   const size_t pad = X->dtype == GGNN_U8 ? 4 : 1;
   size_t want = (size_t)max_batch * (size_t)(X->d + pad) * esz;

@@ -127,13 +127,14 @@ class ShardGroup:
     def search_block(self, Q: np.ndarray, cfg: QueryConfig, buf) -> None:
         """Search every local shard s into block s of `buf`, ids globalized
         (the shards one after the other on this rank's stream)."""
+        up = {}  # the batch is uploaded once for all local shards
         for s, (h, gid) in enumerate(self.shards):
-            self.search_shard(s, h, gid, Q, cfg, buf)
+            self.search_shard(s, h, gid, Q, cfg, buf, up)
 
-    def search_shard(self, s: int, h, gid, Q: np.ndarray, cfg: QueryConfig, buf) -> None:
+    def search_shard(self, s: int, h, gid, Q: np.ndarray, cfg: QueryConfig, buf, uploaded=None) -> None:
         from .shard import search_into_block
 
-        search_into_block(h, Q, cfg, buf, s, self.gid_dev(s))
+        search_into_block(h, Q, cfg, buf, s, self.gid_dev(s), uploaded)
 
     def merge(self, recv, m: int, cfg: QueryConfig):
         from .shard import merge_blocks

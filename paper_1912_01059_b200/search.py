@@ -8,6 +8,7 @@ distances are squared L2; tau is applied in squared space (search.py:45-54).
 
 from __future__ import annotations
 
+import gc
 import threading
 from dataclasses import dataclass
 
@@ -24,7 +25,7 @@ TERMINATED_BY = {0: "stopping-rule", 1: "queue-empty", 2: "iteration-cap"}
 _DISTINCT_CHUNK = 512
 
 
-@dataclass
+@dataclass(slots=True)
 class QueryResult:
     """Ascending (id, distance) results plus search-effort diagnostics."""
 
@@ -62,11 +63,23 @@ class BatchResult:
     def results(self) -> list[QueryResult]:
         """Per-query QueryResult objects; their id / distance arrays are views
         of this batch's (private) host arrays, one row each."""
-        nh = (self.ids >= 0).sum(axis=1).tolist()
+        k = self.ids.shape[1] if self.ids.ndim == 2 else 0
+        nh = (self.ids >= 0).sum(axis=1)
+        ir, dr = list(self.ids), list(self.dists)  # full-row views (C-level), trimmed below where short
+        for i in np.nonzero(nh < k)[0].tolist():
+            ir[i] = ir[i][:nh[i]]
+            dr[i] = dr[i][:nh[i]]
         cnt = self.counters.tolist()
-        ids, dists = self.ids, self.dists
-        return [QueryResult(ids[i, :n], dists[i, :n], c[0], c[1], TERMINATED_BY[c[2]], c[3], c[4])
-                for i, (n, c) in enumerate(zip(nh, cnt))]
+        term = TERMINATED_BY
+        # thousands of small objects: the cyclic collector would run several
+        # times during the list build and find nothing to collect
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            return [QueryResult(ir[i], dr[i], c[0], c[1], term[c[2]], c[3], c[4]) for i, c in enumerate(cnt)]
+        finally:
+            if gc_on:
+                gc.enable()
 
 
 def _params(cfg: QueryConfig, flags: int):
@@ -336,13 +349,21 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
     return BatchResult(ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy())
 
 
-def launch_query(h, queries: np.ndarray, cfg: QueryConfig, ids_p, dists_p, cnt_p) -> None:
+def launch_query(h, queries: np.ndarray, cfg: QueryConfig, ids_p, dists_p, cnt_p, uploaded: dict | None = None) -> None:
     """One ggnn_query_batch launch of every row of `queries` on hierarchy h,
     writing into caller-owned device memory (ids int32 / dists f64 (m, k_out),
-    counters int32 (m, 5)); distinct_touched is not computed."""
+    counters int32 (m, 5)); distinct_touched is not computed.  `uploaded`
+    (a dict the caller keeps) caches the device copy of `queries` per table
+    dtype, so a batch searched on several shards is uploaded once."""
     dh = device_hierarchy(h)
     dv = dh.vectors
-    dq, qs = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
+    key = (dv.dtype, dv.d)
+    hit = uploaded.get(key) if uploaded is not None else None
+    if hit is None:
+        hit = dv.queries(np.ascontiguousarray(queries, dtype=np.float32))
+        if uploaded is not None:
+            uploaded[key] = hit
+    dq, qs = hit
     params = _params(cfg, _qflags(dh, False))
     N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct), N.ptr(dh.top_rows),
            dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max, ids_p, dists_p, cnt_p, None, 0,

@@ -107,12 +107,14 @@ def block_pointers(buf, g: int, m: int, k: int):
     return N.P(base), N.P(base + doff), N.P(base + coff)
 
 
-def search_into_block(h: Hierarchy, Q: np.ndarray, cfg: QueryConfig, buf, g: int, gid_of_local) -> None:
+def search_into_block(h: Hierarchy, Q: np.ndarray, cfg: QueryConfig, buf, g: int, gid_of_local,
+                      uploaded: dict | None = None) -> None:
     """query() of every row of Q on hierarchy h, written into block g of
-    `buf` with ids mapped to dataset ids through gid_of_local (device int32)."""
+    `buf` with ids mapped to dataset ids through gid_of_local (device int32).
+    `uploaded`: the caller's per-batch cache of the device queries."""
     m = Q.shape[0]
     ids_p, dists_p, cnt_p = block_pointers(buf, g, m, cfg.k_out)
-    launch_query(h, Q, cfg, ids_p, dists_p, cnt_p)
+    launch_query(h, Q, cfg, ids_p, dists_p, cnt_p, uploaded)
     N.call("ggnn_shard_globalize", ids_p, m * cfg.k_out, N.ptr(gid_of_local), int(gid_of_local.numel()),
            N.stream_ptr())
 
@@ -138,8 +140,9 @@ def query_sharded_arrays(si: ShardedIndex, queries: np.ndarray, cfg: QueryConfig
     m, G = Q.shape[0], len(si.shards)
     bb = block_layout(m, cfg.k_out)[0]
     buf = N.empty((G * bb,), N.torch().uint8)
+    up = {}  # the batch is uploaded once for all shards
     for g, (_, h) in enumerate(si.shards):
-        search_into_block(h, Q, cfg, buf, g, si.gid_of_local(g))
+        search_into_block(h, Q, cfg, buf, g, si.gid_of_local(g), up)
     ids, dists, cnt = merge_blocks(buf, G, m, cfg.k_out, cfg.k_out)
     if out == "device":
         return ids, dists, cnt

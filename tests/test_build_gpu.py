@@ -290,3 +290,68 @@ def test_leaf_knn_tensor_cores_vs_checker(d):
         p_ref, d_ref = O.batch_bruteforce(X, members[lo:hi], k_nn)
         np.testing.assert_array_equal(pos[lo:hi], p_ref)
         np.testing.assert_array_equal(dist[lo:hi], d_ref)
+
+
+def _leaf_float(X, sizes, rng, k_nn=12):
+    from paper_1912_01059_b200 import _native as N
+    from paper_1912_01059_b200.device import DeviceVectors
+
+    n = X.shape[0]
+    members = rng.permutation(n)[: sizes.sum()].astype(np.int32)
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    dv = DeviceVectors.of_array(X)
+    assert not dv.exact_integers
+    t = N.torch()
+    pos = N.empty((len(members), k_nn), t.int32)
+    dist = N.empty((len(members), k_nn), t.float64)
+    red = t.zeros(1, dtype=t.int32, device=N.device())
+    mem_d, off_d = N.to_dev(members), N.to_dev(offsets)
+    N.call("ggnn_leaf_knn_tc", N.ctypes.byref(dv.struct), N.ptr(mem_d), None, N.ptr(off_d),
+           len(sizes), int(sizes.max()), k_nn, N.ptr(pos), N.ptr(dist), None, 0, None, None, N.ptr(red),
+           N.stream_ptr())
+    pos, dist = pos.cpu().numpy(), dist.cpu().numpy()
+    N.check_tc_timeouts("leaf")
+    assert int(red.item()) == int((sizes < k_nn + 1).sum())
+    for b in range(len(sizes)):
+        lo, hi = offsets[b], offsets[b + 1]
+        p_ref, d_ref = O.batch_bruteforce(X, members[lo:hi], k_nn)
+        np.testing.assert_array_equal(pos[lo:hi], p_ref)
+        np.testing.assert_array_equal(dist[lo:hi], d_ref)
+
+
+@pytest.mark.parametrize("kind", ["gist", "deep", "ties", "offset"])
+def test_leaf_knn_tf32_tensor_cores_vs_checker(kind):
+    """Float leaf kNN on tcgen05 kind::tf32 (3xTF32 Gram matrix of the
+    centred batch, a rigorous error bound selects candidates, sequential FP64
+    re-score): positions and distances bit for bit equal to the reference's
+    batch_bruteforce (CPU checker) on the C3 / C4 generators (gist3k / deep3k
+    rows), on duplicated rows (exact ties) and on rows far from the origin."""
+    rng = np.random.default_rng(len(kind))
+    if kind == "gist":
+        from paper_1912_01059_b200.synthetic import make_latent16
+
+        X = make_latent16(n=3000, d=960, m=1, seed=1234, as_float=True)[0]
+    elif kind == "deep":
+        sys_path_golden()
+        from make_golden import deep_like
+
+        X = deep_like(3000, 1)[0]
+    elif kind == "ties":
+        base = rng.standard_normal((700, 64)).astype(np.float32)
+        X = np.concatenate([base, base[rng.integers(0, 700, size=700)]]).astype(np.float32)
+    else:
+        X = (1000.0 + rng.standard_normal((2000, 40)) * 0.01).astype(np.float32)
+    X = np.ascontiguousarray(X)
+    X.setflags(write=False)
+    sizes = np.concatenate([[2, 3, 16, 17, 128, 127, 64], rng.integers(2, 129, size=9)])
+    sizes = sizes[np.cumsum(sizes) <= X.shape[0]]
+    _leaf_float(X, sizes, rng)
+
+
+def sys_path_golden():
+    import sys
+    from pathlib import Path
+
+    p = str(Path(__file__).resolve().parent / "golden")
+    if p not in sys.path:
+        sys.path.insert(0, p)

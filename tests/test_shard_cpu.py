@@ -34,7 +34,7 @@ class CpuShardGroup(ShardGroup):
     def new_buffer(self, nbytes):
         return torch.zeros(nbytes, dtype=torch.uint8)
 
-    def search_shard(self, s, h, gid, Q, cfg, buf):
+    def search_shard(self, s, h, gid, Q, cfg, buf, uploaded=None):
         m, k = Q.shape[0], cfg.k_out
         bb, doff, coff = block_layout(m, k)
         raw = buf.numpy()[s * bb:(s + 1) * bb]
