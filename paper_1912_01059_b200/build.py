@@ -28,6 +28,7 @@ SYM_CHECK_PRIOQ = 64
 SYM_CHECK_VISITED = 128
 SYM_FALLBACK = 8
 MAX_SLOTS = 32  # adjacency slots per node the kernels handle (ggnn_common.cuh MAX_K)
+CLAIM_CHECK = int(__import__("os").environ.get("GGNN_CLAIM_CHECK", "4"))  # claim rounds per pending read-back
 # node windows per symmetrize pass: requests of x-window w are re-checked after the
 # claims of windows < w, approximating the reference's sequential x order
 # Node windows per symmetrize / merge pass: the reference walks the nodes of a
@@ -327,7 +328,11 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
                    layer.k, layer.k_nn, N.ptr(ws.best), N.ptr(ws.stage), N.ptr(ws.tgt), N.ptr(ws.dropped),
                    N.ptr(ws.pending), x_end, N.ptr(ws.first), N.stream_ptr())
             rounds += 1
-            if x_end == nc and int(ws.pending.item()) == 0:
+            # the open-request count is read back (a host sync) only every
+            # CLAIM_CHECK rounds once every window is active: rounds after the
+            # last request settled are no-ops (every kernel skips settled
+            # requests), so the extra ones cost launches, not results
+            if x_end == nc and (rounds - windows) % CLAIM_CHECK == 0 and int(ws.pending.item()) == 0:
                 break
         layer._version += 1
         dropped = int(ws.dropped.item())

@@ -252,6 +252,10 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
   }
 }
 
+// row gathers through L2 only (ld.global.cg) instead of the read-only L1 path
+#ifndef GGNN_GATHER_CG
+#define GGNN_GATHER_CG 0
+#endif
 template <int LPR, int UNR>
 __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const uint8_t* qs, const int* rows,
                                              int cnt, uint32_t* kout) {
@@ -277,7 +281,7 @@ __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const 
       const uint4 qv = reinterpret_cast<const uint4*>(qs)[c];
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
-        if (rp[u]) v[u] = __ldg(rp[u] + c);
+        if (rp[u]) v[u] = GGNN_GATHER_CG ? __ldcg(rp[u] + c) : __ldg(rp[u] + c);
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
         if (rp[u]) acc[u] += part_u8(v[u], qv);

@@ -113,9 +113,9 @@ struct SearchArgs {
   int32_t* ids;
   double* dists;
   int32_t* counters;
-  uint32_t* ever;       // m * ever_size entries, or nullptr
-  uint32_t ever_size;
-  int ever_cap;         // inserts allowed before a query reports overflow (INT_MAX: exact table)
+  uint32_t* ever;       // distinct_touched logs: m * ever_size entries, or nullptr
+  uint32_t ever_size;   // log capacity per query
+  int32_t* log_len;     // (m) entries logged per query, -1 when the log overflowed
   // query()
   const int32_t* top_rows;
   int64_t ntop;
@@ -236,18 +236,17 @@ __device__ __forceinline__ void init_search(WarpSearch<TX, TQ, LP>& s, const Sea
   s.c = a.c;
   s.target = -1;
   s.carve(region);
-  s.ever = a.ever ? a.ever + (size_t)qi * a.ever_size : nullptr;
-  s.ever_mask = a.ever_size - 1u;
-  s.ever_cap = a.ever_cap;
-  s.ever_overflow = false;
+  s.tlog = a.ever ? a.ever + (size_t)qi * a.ever_size : nullptr;
+  s.log_cap = (int)a.ever_size;
+  s.nlog = 0;
+  s.log_tag = 0u;
 }
 
+// distinct_touched of a search: its log length for the counting pass (-1:
+// overflowed), the counter column holding the part known without the log
 template <typename TX, typename TQ, int LP>
-__device__ __forceinline__ void zero_ever(WarpSearch<TX, TQ, LP>& s, uint32_t size) {
-  if (!s.ever) return;
-  for (uint32_t i = lane_id(); i < size; i += 32) s.ever[i] = 0u;
-  __syncwarp();
-  __threadfence_block();
+__device__ __forceinline__ void finish_log(const WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64_t qi) {
+  if (a.ever && lane_id() == 0) a.log_len[qi] = s.nlog <= s.log_cap ? s.nlog : -1;
 }
 
 template <typename TX, typename TQ, int LP>
@@ -272,9 +271,10 @@ __device__ void write_hits(WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64
     c[0] = s.visited + extra_visited;
     c[1] = s.steps;
     c[2] = s.term;
-    c[3] = (a.ever == nullptr || s.ever_overflow) ? -1 : s.distinct + extra_distinct;
+    c[3] = a.ever == nullptr ? -1 : extra_distinct;  // + the log's distinct ids (distinct_log_kernel)
     c[4] = s.forgotten;
   }
+  finish_log(s, a, qi);
 }
 
 // Fused exchange: this query's row, ids globalized, into block push_rank of
@@ -312,7 +312,6 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
   set_layer(s, a.layer);
   s.dmax = a.dmax;
   s.reset();
-  zero_ever(s, a.ever_size);
   // top_layer_seeds (search.py:100-112): exact top-min(k_out, ntop) over the
   // top layer, 32 ranks per pass (one pass unless k_out and the top layer
   // both exceed 32)
@@ -369,7 +368,6 @@ __device__ __forceinline__ void greedy_kernel_one(const SearchArgs& a, uint8_t* 
   set_layer(s, a.layer);
   s.dmax = a.dmax;
   s.reset();
-  zero_ever(s, a.ever_size);
   for (int base = 0; base < a.nseeds; base += 32) {
     const int cnt = min(32, a.nseeds - base);
     int sid = -1;
@@ -417,8 +415,9 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     hi = min(lo + a.seg_size, (int)Ls.node_count);
   }
   const int kk = min(a.c.k_out, hi - lo);
+  // distinct_touched: the scanned rows not seeded, plus every layer search's
+  // logged ids (tagged by layer) counted after the launch
   int visited = hi - lo, steps = 0, distinct = (hi - lo) - kk, forgotten = 0, term = TERM_EMPTY;
-  bool ever_ovf = false;
   if (a.c.k_out <= 32) {  // hits fit the lanes: carried between layers in registers
     Key bk;
     int bi;
@@ -430,13 +429,11 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
       const int sid = lane < nh ? __ldg(a.layers[j + 1].down + id) : -1;
       set_layer(s, Lj);
       s.reset();
-      zero_ever(s, a.ever_size);
+      s.log_tag = (uint32_t)j << 27;
       s.seed(bk, sid, nh);
       s.run();
       visited += s.visited;
       steps += s.steps;
-      distinct += s.distinct;
-      ever_ovf = ever_ovf || s.ever_overflow;
       forgotten += s.forgotten;
       term = s.term;
       nh = s.hits(bk, id);
@@ -444,8 +441,10 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     if (a.start == a.stop) {  // no search ran: the segment's top-kk goes into the ring for write_out
       set_layer(s, Ls);
       s.reset();
-      s.ever = nullptr;  // (its table is not zeroed; the count is `distinct` above)
+      uint32_t* const tl = s.tlog;
+      s.tlog = nullptr;  // placing the scan's result is not a search (counted in `distinct` above)
       s.seed(bk, id, nh);
+      s.tlog = tl;
     }
   } else {
     // k_out > 32: the segment scan in passes of 32 ranks seeds the ring of
@@ -453,8 +452,8 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     // (stash) while the next layer's search is seeded from them
     set_layer(s, Ls);
     s.reset();
-    uint32_t* const ever = s.ever;
-    s.ever = nullptr;  // seeding the scan's result is not a search: no distinct-set yet
+    uint32_t* const tl = s.tlog;
+    s.tlog = nullptr;  // placing the scan's result is not a search (counted in `distinct` above)
     Key ak = 0;
     int ai = -1;
     for (int b = 0; b < kk; b += 32) {
@@ -466,14 +465,14 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
       ai = __shfl_sync(FULL, bi, kc - 1);
       s.seed(bk, lane < kc ? bi + lo : -1, kc);
     }
-    s.ever = ever;
+    s.tlog = tl;
     for (int j = a.start - 1; j >= a.stop; --j) {
       const int nh = min(s.L, a.c.k_out);
       s.stash(nh);
       const int32_t* down = a.layers[j + 1].down;
       set_layer(s, a.layers[j]);
       s.reset();
-      zero_ever(s, a.ever_size);
+      s.log_tag = (uint32_t)j << 27;
       for (int b = 0; b < nh; b += 32) {
         Key sk = KeyOps<Key>::max_key();
         int sid = -1;
@@ -487,8 +486,6 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
       s.run();
       visited += s.visited;
       steps += s.steps;
-      distinct += s.distinct;
-      ever_ovf = ever_ovf || s.ever_overflow;
       forgotten += s.forgotten;
       term = s.term;
     }
@@ -502,9 +499,10 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
     c[0] = visited;
     c[1] = steps;
     c[2] = term;
-    c[3] = (a.ever == nullptr || ever_ovf) ? -1 : distinct;
+    c[3] = a.ever == nullptr ? -1 : distinct;  // + the log's distinct ids (distinct_log_kernel)
     c[4] = forgotten;
   }
+  finish_log(s, a, qi);
 }
 
 template <typename TX, typename TQ, int LP>
@@ -612,10 +610,10 @@ __device__ __forceinline__ void symcheck_kernel_one(const SymArgs& a, uint8_t* s
     s.c = a.c;
     s.target = x;
     s.carve(smem_w);
-    s.ever = nullptr;
-    s.ever_mask = 0;
-    s.ever_cap = INT_MAX;
-    s.ever_overflow = false;
+    s.tlog = nullptr;
+    s.log_cap = 0;
+    s.nlog = 0;
+    s.log_tag = 0u;
     set_layer(s, a.layer);
     s.dmax = a.dmax;
     const int xrow = a.layer.to_row ? __ldg(a.layer.to_row + x) : x;
@@ -920,35 +918,94 @@ int combo(const ggnn_vectors* X, const ggnn_queries* Q) {
   return qd == GGNN_U8 ? 1 : 2;                // u8 / u8, u8 / f32
 }
 
-// Exact distinct_touched needs a per-query set of every id touched; a table
-// for the worst case (max_iterations * k touches) is 256 KB per query at the
-// defaults, while typical searches touch ~1-2 k ids.  ggnn_search_workspace_bytes
-// therefore asks for COMPACT_EVER entries per query; a query that fills 3/4 of
-// it stops counting and reports distinct_touched = -1, and the caller reruns
-// just those queries with a workspace of the exact size (attach_ever picks
-// the exact table whenever the workspace holds one).
-constexpr uint32_t COMPACT_EVER = 4096;
+// Exact distinct_touched: each search appends every id it inserts to a
+// per-query log in the workspace (no atomics, nothing on the search's
+// critical path waits on it) and distinct_log_kernel counts the distinct
+// entries after the launch.  ggnn_search_workspace_bytes asks for COMPACT_LOG
+// entries per query (typical searches log ~1-2 k); a longer log reports
+// distinct_touched = -1 and the caller reruns those queries with a workspace
+// of the exact size (attach_ever takes whatever capacity the workspace holds).
+constexpr uint32_t COMPACT_LOG = 4096;
+constexpr uint32_t LOG_SMEM_SLOTS = 32768;  // counting table in shared memory up to this size
 
-uint32_t ever_size_for(const ggnn_search_params* p, int32_t max_seeds, int k) {
-  uint64_t need = 2ull * ((uint64_t)max_seeds + (uint64_t)std::max<int64_t>(p->max_iterations, 1) * (uint64_t)k) + 64;
-  uint32_t e = 64;
-  while (e < need && e < (1u << 30)) e <<= 1;
-  return e;
+uint32_t log_entries_for(const ggnn_search_params* p, int32_t max_seeds, int k) {
+  // one layer's search inserts at most its seeds plus k ids per step; twice
+  // that also covers a descent's coarse layers (a longer log reports -1)
+  const uint64_t one = (uint64_t)std::max(max_seeds, 0) + (uint64_t)std::max<int64_t>(p->max_iterations, 1) * k;
+  return (uint32_t)std::min<uint64_t>(2 * one + 64, 1u << 28);
 }
 
+size_t log_bytes(int64_t m, uint32_t cap) { return (size_t)m * cap * 4 + (size_t)m * 4; }
+
 int attach_ever(SearchArgs& a, const ggnn_search_params* p, int32_t max_seeds, int k, void* ws, size_t wsb) {
-  a.ever_cap = INT_MAX;
-  if (!(p->flags & GGNN_FLAG_DISTINCT)) return GGNN_OK;
-  const uint32_t full = ever_size_for(p, max_seeds, k);
-  const uint32_t small = std::min(full, COMPACT_EVER);
-  const size_t per = a.m > 0 ? wsb / ((size_t)a.m * 4) : 0;
-  GGNN_CHECK_ARG(ws != nullptr && per >= small, "GGNN_FLAG_DISTINCT needs %zu bytes of workspace (exact: %zu)",
-                 (size_t)a.m * small * 4, (size_t)a.m * full * 4);
-  uint32_t e = small;
-  while (e < full && (size_t)e * 2 <= per) e <<= 1;
+  if (!(p->flags & GGNN_FLAG_DISTINCT) || a.m <= 0) return GGNN_OK;
+  const uint32_t full = log_entries_for(p, max_seeds, k);
+  const uint32_t small = std::min(full, COMPACT_LOG);
+  GGNN_CHECK_ARG(ws != nullptr && wsb >= log_bytes(a.m, small),
+                 "GGNN_FLAG_DISTINCT needs %zu bytes of workspace (exact: %zu)", log_bytes(a.m, small),
+                 log_bytes(a.m, full));
+  const size_t per = (wsb - (size_t)a.m * 4) / ((size_t)a.m * 4);
   a.ever = reinterpret_cast<uint32_t*>(ws);
-  a.ever_size = e;
-  a.ever_cap = e >= full ? INT_MAX : (int)(e / 4 * 3);
+  a.ever_size = (uint32_t)std::min<size_t>(per, full);
+  a.log_len = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + (size_t)a.m * a.ever_size * 4);
+  return GGNN_OK;
+}
+
+// One CTA per query: insert its logged ids into an open-addressing set (shared
+// memory, or global scratch for very long logs) and add the number of new
+// ones to counter column 3; an overflowed log gives -1.
+__global__ void __launch_bounds__(256) distinct_log_kernel(const uint32_t* logs, const int32_t* len, uint32_t cap,
+                                                           int32_t* counters, uint32_t slots, uint32_t* gtab) {
+  extern __shared__ uint32_t tab_s[];
+  __shared__ int total;
+  const int64_t qi = blockIdx.x;
+  const int n = len[qi];
+  if (n < 0) {
+    if (threadIdx.x == 0) counters[qi * 5 + 3] = -1;
+    return;
+  }
+  uint32_t* tab = gtab ? gtab + (size_t)qi * slots : tab_s;
+  for (uint32_t i = threadIdx.x; i < slots; i += blockDim.x) tab[i] = 0u;
+  if (threadIdx.x == 0) total = 0;
+  __syncthreads();
+  const uint32_t* lg = logs + (size_t)qi * cap;
+  const uint32_t mask = slots - 1u;
+  int fresh = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t key = lg[i] + 1u;
+    uint32_t h = (key * 2654435761u) & mask;
+    for (;;) {
+      const uint32_t o = atomicCAS(&tab[h], 0u, key);
+      if (o == 0u) {
+        ++fresh;
+        break;
+      }
+      if (o == key) break;
+      h = (h + 1u) & mask;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fresh += __shfl_xor_sync(FULL, fresh, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&total, fresh);
+  __syncthreads();
+  if (threadIdx.x == 0) counters[qi * 5 + 3] += total;
+}
+
+int count_distinct(const SearchArgs& a, cudaStream_t st) {
+  if (!a.ever || !a.counters || a.m <= 0) return GGNN_OK;
+  uint32_t slots = 64;
+  while ((uint64_t)slots * 3 < (uint64_t)a.ever_size * 4) slots <<= 1;  // load <= 3/4
+  uint32_t* g = nullptr;
+  size_t smem = (size_t)slots * 4;
+  if (slots > LOG_SMEM_SLOTS) {
+    GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&g), (size_t)a.m * slots * 4, st));
+    smem = 0;
+  } else {
+    GGNN_CUDA_TRY(cudaFuncSetAttribute(distinct_log_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  distinct_log_kernel<<<(unsigned)a.m, 256, smem, st>>>(a.ever, a.log_len, a.ever_size, a.counters, slots, g);
+  GGNN_LAUNCH_CHECK();
+  if (g) GGNN_CUDA_TRY(cudaFreeAsync(g, st));
   return GGNN_OK;
 }
 
@@ -973,10 +1030,10 @@ int ggnn_device_info(int* sm_count, int* smem_per_block) {
 
 size_t ggnn_search_workspace_bytes(int64_t m, const ggnn_search_params* p, int32_t max_seeds) {
   if (!p || !(p->flags & GGNN_FLAG_DISTINCT)) return 0;
-  // max_seeds < 0: room for the exact table of every query (any seed count <= max(32, k_out))
-  const uint32_t full = ever_size_for(p, max_seeds < 0 ? std::max(32, p->k_out) : max_seeds, MAX_K);
-  if (max_seeds < 0) return (size_t)m * full * 4;
-  return (size_t)m * std::min(full, COMPACT_EVER) * 4;
+  // max_seeds < 0: room for the exact log of every query (any seed count <= max(32, k_out))
+  const uint32_t full = log_entries_for(p, max_seeds < 0 ? std::max(32, p->k_out) : max_seeds, MAX_K);
+  if (max_seeds < 0) return log_bytes(m, full);
+  return log_bytes(m, std::min(full, COMPACT_LOG));
 }
 
 __global__ void rows_unique_kernel(const int32_t* adj, int64_t node_count, int k, int32_t* result) {
@@ -1032,10 +1089,11 @@ int ggnn_query_batch(const ggnn_vectors* X, const ggnn_layer* bottom, const int3
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return GGNN_LAUNCH_LP(query_kernel, float, float, a, a.m, a.region, st);
-    case 1: return GGNN_LAUNCH_LP(query_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
-    default: return launch_warps(query_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
+    case 0: rc = GGNN_LAUNCH_LP(query_kernel, float, float, a, a.m, a.region, st); break;
+    case 1: rc = GGNN_LAUNCH_LP(query_kernel, uint8_t, uint8_t, a, a.m, a.region, st); break;
+    default: rc = launch_warps(query_kernel<uint8_t, float, 0>, a, a.m, a.region, st); break;
   }
+  return rc ? rc : count_distinct(a, st);
 }
 
 int ggnn_query_batch_push(const ggnn_vectors* X, const ggnn_layer* bottom, const int32_t* d_top_rows, int64_t ntop,
@@ -1058,7 +1116,6 @@ int ggnn_query_batch_push(const ggnn_vectors* X, const ggnn_layer* bottom, const
   a.ids = d_ids;
   a.dists = d_dists;
   a.counters = d_counters;
-  a.ever_cap = INT_MAX;
   const size_t bb = ggnn_shard_block_bytes(a.m, p->k_out);
   const size_t half = (size_t)push->nranks * bb + (((size_t)push->nranks * 4 + 255) & ~size_t(255));
   for (int g = 0; g < push->nranks; ++g) {
@@ -1113,7 +1170,6 @@ int ggnn_query_batch_staged(const ggnn_vectors* X, const ggnn_layer* bottom, con
   a.ids = d_ids;
   a.dists = d_dists;
   a.counters = d_counters;
-  a.ever_cap = INT_MAX;
   a.qflags = d_chunk_flags;
   a.qchunk = chunk_rows;
   a.qepoch = epoch;
@@ -1196,10 +1252,11 @@ int ggnn_greedy_batch(const ggnn_vectors* X, const ggnn_layer* layer, const ggnn
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return GGNN_LAUNCH_LP(greedy_kernel, float, float, a, a.m, a.region, st);
-    case 1: return GGNN_LAUNCH_LP(greedy_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
-    default: return launch_warps(greedy_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
+    case 0: rc = GGNN_LAUNCH_LP(greedy_kernel, float, float, a, a.m, a.region, st); break;
+    case 1: rc = GGNN_LAUNCH_LP(greedy_kernel, uint8_t, uint8_t, a, a.m, a.region, st); break;
+    default: rc = launch_warps(greedy_kernel<uint8_t, float, 0>, a, a.m, a.region, st); break;
   }
+  return rc ? rc : count_distinct(a, st);
 }
 
 int ggnn_descent_batch(const ggnn_vectors* X, const ggnn_layer* layers, int32_t num_layers, int32_t start,
@@ -1217,6 +1274,9 @@ int ggnn_descent_batch(const ggnn_vectors* X, const ggnn_layer* layers, int32_t 
     if (j > stop && j <= start) GGNN_CHECK_ARG(layers[j].d_down != nullptr, "layer %d needs a down map", j);
     a.layers[j] = to_dev(layers[j]);
   }
+  if (p->flags & GGNN_FLAG_DISTINCT)  // distinct_touched logs tag ids with their layer (bits 27..31)
+    for (int j = stop; j <= start; ++j)
+      GGNN_CHECK_ARG(layers[j].node_count < (1 << 27), "distinct_touched on descents needs layers below 2^27 nodes");
   a.start = start;
   a.stop = stop;
   a.seg_lo = d_seg_lo;
@@ -1228,10 +1288,11 @@ int ggnn_descent_batch(const ggnn_vectors* X, const ggnn_layer* layers, int32_t 
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
-    case 0: return GGNN_LAUNCH_LP(descent_kernel, float, float, a, a.m, a.region, st);
-    case 1: return GGNN_LAUNCH_LP(descent_kernel, uint8_t, uint8_t, a, a.m, a.region, st);
-    default: return launch_warps(descent_kernel<uint8_t, float, 0>, a, a.m, a.region, st);
+    case 0: rc = GGNN_LAUNCH_LP(descent_kernel, float, float, a, a.m, a.region, st); break;
+    case 1: rc = GGNN_LAUNCH_LP(descent_kernel, uint8_t, uint8_t, a, a.m, a.region, st); break;
+    default: rc = launch_warps(descent_kernel<uint8_t, float, 0>, a, a.m, a.region, st); break;
   }
+  return rc ? rc : count_distinct(a, st);
 }
 
 int ggnn_merge_descent(const ggnn_vectors* X, const ggnn_layer* layers, int32_t num_layers, int32_t start,

@@ -98,6 +98,11 @@ inline int table_log2(int cap, int vsz) {
 #define GGNN_PREFETCH_LINES 1
 #endif
 constexpr int PREFETCH_LINES = GGNN_PREFETCH_LINES;
+// prefetch into L2 only (the L1 left beside 28 searches' shared memory is
+// small: ncu measures a 2 % L1 hit rate for the row gathers)
+#ifndef GGNN_PREFETCH_L2
+#define GGNN_PREFETCH_L2 0
+#endif
 
 template <typename Key>
 __device__ void warp_sorted_out(const Key* keys, const int* ids, int n, int K, int32_t* out_ids, double* out_d);
@@ -133,12 +138,15 @@ struct WarpSearch {
   int* crow;
   int* cid;
   Key* ckey;
-  // diagnostic ever-set (global): the ids this search touched, for the exact
-  // distinct_touched; a compact table gives up (ever_overflow) past ever_cap
-  uint32_t* ever;
-  uint32_t ever_mask;
-  int ever_cap;
-  bool ever_overflow;
+  // distinct_touched log (FLAG_DISTINCT): every id the search inserts --
+  // seeds and computed candidates -- is appended to a per-query list in
+  // global memory with plain stores that nothing waits on; a pass after the
+  // search counts the distinct entries (distinct_log_kernel).  log_tag keeps
+  // the ids of different layers apart (descents: layer << 27).
+  uint32_t* tlog;
+  int log_cap;
+  int nlog;
+  uint32_t log_tag;
   // warp-uniform state
   int L, vlen, vpos, used, rebuild_at;
   // adjacency row of the predicted next expansion, loaded while the current
@@ -189,28 +197,12 @@ struct WarpSearch {
     found_target = false;
   }
 
-  __device__ __forceinline__ int ever_insert(int id) {
-    if (id < 0 || ever == nullptr) return 0;
-    uint32_t key = (uint32_t)id + 1u;
-    uint32_t s = (key * 2654435761u) & ever_mask;
-    for (;;) {
-      uint32_t v = ever[s];
-      if (v == key) return 0;
-      if (v == 0u) {
-        uint32_t o = atomicCAS(&ever[s], 0u, key);
-        if (o == 0u) return 1;
-        if (o == key) return 0;
-        continue;
-      }
-      s = (s + 1) & ever_mask;
-    }
-  }
-
-  __device__ __forceinline__ void check_ever() {
-    if (distinct > ever_cap) {  // compact table 3/4 full: stop, report -1
-      ever_overflow = true;
-      ever = nullptr;
-    }
+  // append lanes [0, n) with valid[lane] to the log (in lane order)
+  __device__ __forceinline__ void log_lanes(bool valid, int id) {
+    const unsigned vm = __ballot_sync(FULL, valid);
+    const int pos = nlog + __popc(vm & lanemask_lt());
+    if (valid && pos < log_cap) tlog[pos] = log_tag | (uint32_t)id;
+    nlog += __popc(vm);
   }
 
   __device__ __forceinline__ int warp_sum(int v) {
@@ -419,11 +411,8 @@ struct WarpSearch {
       id = INT_MAX;
     }
     const int cnt = __popc(__ballot_sync(FULL, v));
-    if (ever) {
-      distinct += __popc(__ballot_sync(FULL, ever_insert(v ? id : -1) != 0));
-      check_ever();
-    }
-    else distinct += cnt;
+    if (tlog) log_lanes(v, id);
+    distinct += cnt;
     warp_sort_n(key, id, n);  // valid seeds sit anywhere in lanes [0, n): bitonic
     if (cnt) merge(key, id, cnt);
     next_head = -2;
@@ -472,7 +461,10 @@ struct WarpSearch {
         const char* rp = reinterpret_cast<const char*>(X + (int64_t)nrow * d);
 #pragma unroll
         for (int l = 0; l < PREFETCH_LINES; ++l)
-          if (l * 128 < d * (int64_t)sizeof(TX)) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + l * 128));
+          if (l * 128 < d * (int64_t)sizeof(TX)) {
+            if (GGNN_PREFETCH_L2) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + l * 128));
+            else asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + l * 128));
+          }
       }
     }
     bool cand = nb >= 0;
@@ -501,10 +493,7 @@ struct WarpSearch {
       }
       __syncwarp();
       visited += nc;
-      if (ever) {
-        distinct += __popc(__ballot_sync(FULL, ever_insert(lane < nc ? id : -1) != 0));
-        check_ever();
-      }
+      if (tlog) log_lanes(lane < nc, id);
       int m;
       if (PACK && d <= 33000) {  // u8 keys (d * 255^2) stay below 2^31
         // admission first, then rank only what is admitted: every rejected

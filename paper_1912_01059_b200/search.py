@@ -223,16 +223,17 @@ def _query_host_staged(dh, Q: np.ndarray, cfg: QueryConfig):
 _HOST_LOCK = threading.Lock()
 
 
-def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
+def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig, distinct: bool = False) -> BatchResult:
     with _HOST_LOCK:
-        return _query_host_fast_locked(dh, Q, cfg)
+        return _query_host_fast_locked(dh, Q, cfg, distinct)
 
 
-def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
+def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig, distinct: bool = False) -> BatchResult:
     t = N.torch()
     # staged: uint8 tables only (float32 rows stay float and their upload is
-    # 4x larger; measured slower than the chunked path on gist1m)
-    if _STAGED and Q.shape[0] >= 1024 and dh.vectors.exact_integers:
+    # 4x larger; measured slower than the chunked path on gist1m), and no
+    # distinct_touched logs
+    if _STAGED and not distinct and Q.shape[0] >= 1024 and dh.vectors.exact_integers:
         r = _query_host_staged(dh, Q, cfg)
         if r is not None:
             return r
@@ -245,7 +246,7 @@ def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
     if streams is None:
         streams = _STREAMS[dev] = (t.cuda.Stream(), t.cuda.Stream())
     main = t.cuda.current_stream()
-    params = _params(cfg, _qflags(dh, False))
+    params = _params(cfg, _qflags(dh, distinct))
     nchunks = max(1, min(_CHUNKS, m // 1024))
     if nchunks > 1:
         first = max(1, min(m - 1, int(m * _FIRST)))
@@ -272,9 +273,10 @@ def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
                 qs = N.queries_struct(data=st.q_u8[lo:hi], dtype_code=N.GGNN_U8, m=hi - lo)
             else:
                 qs = N.queries_struct(data=st.q_f32[lo:hi], dtype_code=N.GGNN_F32, m=hi - lo)
+            ws, wsb = _workspace(hi - lo, params, cfg.k_out)  # distinct_touched logs (or none)
             N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
                    N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max,
-                   N.ptr(st.ids[lo:hi]), N.ptr(st.dists[lo:hi]), N.ptr(st.cnt[lo:hi]), None, 0, sp)
+                   N.ptr(st.ids[lo:hi]), N.ptr(st.dists[lo:hi]), N.ptr(st.cnt[lo:hi]), N.ptr(ws), wsb, sp)
             st.ids_pin[lo:hi].copy_(st.ids[lo:hi], non_blocking=True)
             st.dists_pin[lo:hi].copy_(st.dists[lo:hi], non_blocking=True)
             st.cnt_pin[lo:hi].copy_(st.cnt[lo:hi], non_blocking=True)
@@ -289,9 +291,10 @@ def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
         # some query is not integral: the uint8 searches above are void; search
         # the float batch (already on the device) against the uint8 table
         qs = N.queries_struct(data=st.q_f32, dtype_code=N.GGNN_F32, m=m)
+        ws, wsb = _workspace(m, params, cfg.k_out)
         N.call("ggnn_query_batch", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
                N.ptr(dh.top_rows), dh.ntop, N.ctypes.byref(qs), N.ctypes.byref(params), dh.d_nn1_max,
-               N.ptr(st.ids), N.ptr(st.dists), N.ptr(st.cnt), None, 0, N.stream_ptr())
+               N.ptr(st.ids), N.ptr(st.dists), N.ptr(st.cnt), N.ptr(ws), wsb, N.stream_ptr())
         st.ids_pin[:m].copy_(st.ids[:m], non_blocking=True)
         st.dists_pin[:m].copy_(st.dists[:m], non_blocking=True)
         st.cnt_pin[:m].copy_(st.cnt[:m], non_blocking=True)
@@ -301,10 +304,12 @@ def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig) -> BatchResult:
 
 
 def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinct: bool = False,
-                 out: str = "numpy"):
+                 out: str = "numpy", _exact: bool = False):
     """Batched query(): top-layer scan + best-first search on layer 0 for every
     row of `queries` in one launch.  Returns a BatchResult (host arrays) or,
-    with out="device", the device tensors (ids, dists, counters)."""
+    with out="device", the device tensors (ids, dists, counters).
+    distinct=True also computes distinct_touched (counter column 3; -1
+    otherwise)."""
     cfg = cfg or QueryConfig()
     dh = device_hierarchy(h)
     dv = dh.vectors
@@ -313,8 +318,14 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
         Q = Q[None, :]
     if Q.shape[1] != dv.d:
         raise ValueError(f"query dimension {Q.shape[1]} does not match index dimension {dv.d}")
-    if not distinct and out == "numpy" and Q.shape[0] > 0:
-        return _query_host_fast(dh, Q, cfg)
+    if out == "numpy" and Q.shape[0] > 0:
+        res = _query_host_fast(dh, Q, cfg, distinct)
+        redo = np.nonzero(res.counters[:, 3] < 0)[0] if distinct else ()
+        for lo in range(0, len(redo), _DISTINCT_CHUNK):  # compact logs that overflowed: exact reruns
+            sel = redo[lo:lo + _DISTINCT_CHUNK]
+            sub = query_arrays(h, Q[sel], cfg, distinct=True, out="device", _exact=True)
+            res.ids[sel], res.dists[sel], res.counters[sel] = (x.cpu().numpy() for x in sub)
+        return res
     m = Q.shape[0]
     t = N.torch()
     ids = N.empty((m, cfg.k_out), t.int32)
@@ -330,8 +341,8 @@ def query_arrays(h, queries: np.ndarray, cfg: QueryConfig | None = None, distinc
                dh.ntop, N.ctypes.byref(sub_q), N.ctypes.byref(params), dh.d_nn1_max, out_ids, out_d, out_c,
                N.ptr(ws), wsb, N.stream_ptr())
 
-    launch(0, m, qs, N.ptr(ids), N.ptr(dists), N.ptr(cnt), False)
-    if distinct and m:
+    launch(0, m, qs, N.ptr(ids), N.ptr(dists), N.ptr(cnt), _exact)
+    if distinct and m and not _exact:
         # queries whose compact distinct-set overflowed (distinct_touched = -1)
         # run again with exact per-query tables, a few at a time
         redo = np.nonzero(cnt[:, 3].cpu().numpy() < 0)[0]
