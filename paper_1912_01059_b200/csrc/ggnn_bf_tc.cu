@@ -339,8 +339,13 @@ int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_i
 
 }  // namespace ggnn
 
+namespace ggnn {
+int bf_tf32_timeouts();  // ggnn_bf_tf32.cu
+}
+
 extern "C" int ggnn_bf_timeouts(void) {
   int v = 0;
   if (cudaMemcpyFromSymbol(&v, ggnn::g_bf_timeouts, sizeof(int)) != cudaSuccess) return -1;
-  return v;
+  const int w = ggnn::bf_tf32_timeouts();
+  return w < 0 ? -1 : v + w;
 }

@@ -22,6 +22,13 @@ namespace ggnn {
 bool bf_tc_eligible(const ggnn_vectors* X, const int32_t* d_rows, const ggnn_queries* Q, int k);
 int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_ids, double* d_dists,
                cudaStream_t st);
+// tensor-core brute force for float tables (ggnn_bf_tf32.cu)
+bool bf_tf32_eligible(const ggnn_vectors* X, const int32_t* d_rows, const ggnn_queries* Q, int k);
+int bf_topk_tf32(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_ids, double* d_dists,
+                 cudaStream_t st);
+struct SearchArgs;
+int exhaustive_warp(SearchArgs& a, const ggnn_vectors* X, const ggnn_queries* Q, const int32_t* d_rows, int64_t nrows,
+                    int32_t* d_ids, double* d_dists, cudaStream_t st);
 
 static thread_local std::string g_err;
 // ggnn_search_accounting: (visited, steps) totals of the build-type searches
@@ -1430,10 +1437,21 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   int rc = fill_common(a, X, Q, &p);
   if (rc) return rc;
   GGNN_CHECK_ARG(nrows >= 1 && nrows <= INT32_MAX, "invalid row count");
-  // whole-table scans of uint8 data at least one X tile per split long: tensor cores
+  // whole-table scans at least one X tile per split long: tensor cores
+  // (kind::i8 for uint8 tables, 3xTF32 + exact re-score for float tables)
   if (bf_tc_eligible(X, d_rows, Q, k) && nrows == X->n && X->n >= 4096)
     return bf_topk_tc(X, Q, k, d_ids, d_dists, as_stream(stream));
-  // otherwise the warp scan, ceil(k / 32) passes over the rows
+  if (bf_tf32_eligible(X, d_rows, Q, k) && nrows == X->n)
+    return bf_topk_tf32(X, Q, k, d_ids, d_dists, as_stream(stream));
+  return exhaustive_warp(a, X, Q, d_rows, nrows, d_ids, d_dists, as_stream(stream));
+}
+
+}  // extern "C"
+
+namespace ggnn {
+// the CUDA-core scan (any k, ceil(k / 32) passes over the rows)
+int exhaustive_warp(SearchArgs& a, const ggnn_vectors* X, const ggnn_queries* Q, const int32_t* d_rows, int64_t nrows,
+                    int32_t* d_ids, double* d_dists, cudaStream_t st) {
   a.top_rows = d_rows;
   a.ntop = nrows;
   a.ids = d_ids;
@@ -1441,7 +1459,6 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
   int qd = Q->d_rows ? X->dtype : Q->dtype;
   int keysize = (X->dtype == GGNN_U8 && qd == GGNN_U8) ? 4 : 8;
   a.region = 128 + align16(32 * (size_t)keysize) + align16((size_t)X->d * qelem_of(qd));
-  cudaStream_t st = as_stream(stream);
   switch (combo(X, Q)) {
     case 0:
       if (a.lpr == 32) return launch_static(topk_kernel<float, float, 32>, a, a.m, a.region, st, 8);
@@ -1454,6 +1471,19 @@ int ggnn_exhaustive_topk(const ggnn_vectors* X, const int32_t* d_rows, int64_t n
     default: return launch_static(topk_kernel<uint8_t, float, 0>, a, a.m, a.region, st, 8);
   }
 }
+
+int topk_scan_subset(const ggnn_vectors* X, const float* Qsub, int64_t cnt, int k, int32_t* ids, double* dists,
+                     cudaStream_t st) {
+  ggnn_queries q{Qsub, nullptr, cnt, GGNN_F32, 0};
+  ggnn_search_params p{k, k, 1, 0, 0.0, 0};
+  SearchArgs a;
+  int rc = fill_common(a, X, &q, &p);
+  if (rc) return rc;
+  return exhaustive_warp(a, X, &q, nullptr, X->n, ids, dists, st);
+}
+}  // namespace ggnn
+
+extern "C" {
 
 int ggnn_exhaustive_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int32_t k, int32_t* d_ids,
                             double* d_dists, void* stream) {

@@ -355,3 +355,31 @@ def sys_path_golden():
     p = str(Path(__file__).resolve().parent / "golden")
     if p not in sys.path:
         sys.path.insert(0, p)
+
+
+def test_build_accounting_counts_every_search():
+    """ggnn_search_accounting: the device totals equal the sum of the
+    searches' own (visited, steps) counters, and build(..., accounting=True)
+    reports per-phase algorithmic bytes (SURVEY 8d build accounting)."""
+    from paper_1912_01059_b200 import _native as N
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, Q = make_latent16(n=4000, d=32, m=300, seed=2)
+    h, st = ga.build(ga.Dataset(base), ga.BuildConfig(seed=7), accounting=True)
+    summ = st.accounting_summary(32, 1)
+    assert summ["visited_total"] > 0 and summ["steps_total"] > 0 and summ["leaf_knn_flops"] > 0
+    assert summ["search_bytes_total"] == sum(
+        v * 32 + st.search_steps[k] * (4 * 24 + 4) for k, v in st.search_visited.items())
+    t = N.torch()
+    acc = t.zeros(2, dtype=t.int64, device=N.device())
+    N.call("ggnn_search_accounting", N.ptr(acc))
+    try:
+        res = ga.search.descent_arrays(h, Q, ga.QueryConfig(k_out=10, tau=0.6), h.num_layers - 1, 0)
+    finally:
+        N.call("ggnn_search_accounting", None)
+    v, s = acc.tolist()
+    assert v == int(res.counters[:, 0].astype(np.int64).sum())
+    assert s == int(res.counters[:, 1].astype(np.int64).sum())
+    # off again: nothing more is counted
+    ga.search.descent_arrays(h, Q, ga.QueryConfig(k_out=10, tau=0.6), h.num_layers - 1, 0)
+    assert acc.tolist() == [v, s]

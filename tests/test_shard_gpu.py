@@ -362,3 +362,43 @@ def test_bruteforce_tensor_cores_large_k(k):
         ri, rd = O.exhaustive_topk(X[:1000], Q[i], k)
         np.testing.assert_array_equal(small.ids[i], ri)
         np.testing.assert_array_equal(small.dists[i], rd)
+
+
+@pytest.mark.parametrize("kind,k", [("normal", 10), ("dups", 32), ("gist", 10), ("offset", 1)])
+def test_bruteforce_tf32_tensor_cores_vs_checker(kind, k):
+    """Float tables on tcgen05 kind::tf32 (3xTF32 Gram of centred rows, a
+    rigorous error bound selects candidates, sequential FP64 re-score): the
+    exhaustive top-k equals the reference's exhaustive_topk (CPU checker, ties
+    by row) bit for bit -- including duplicated rows (exact ties), the C3
+    generator at d = 960, and rows far from the origin."""
+    rng = np.random.default_rng(len(kind) * 10 + k)
+    if kind == "normal":
+        X = rng.standard_normal((9001, 64)).astype(np.float32)
+        Q = rng.standard_normal((300, 64)).astype(np.float32)
+    elif kind == "dups":
+        base = rng.standard_normal((3000, 32)).astype(np.float32)
+        X = np.concatenate([base, base, base[:2000]])
+        Q = base[rng.integers(0, 3000, size=200)] + np.float32(0.01) * rng.standard_normal((200, 32)).astype(np.float32)
+    elif kind == "gist":
+        from paper_1912_01059_b200.synthetic import make_latent16
+
+        X, Q = make_latent16(n=6000, d=960, m=64, seed=7, as_float=True)
+    else:
+        X = (500.0 + rng.standard_normal((5000, 24)) * 0.05).astype(np.float32)
+        Q = (500.0 + rng.standard_normal((100, 24)) * 0.05).astype(np.float32)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    Q = np.ascontiguousarray(Q, dtype=np.float32)
+    gt = ga.brute_force_oracle(ga.Dataset(X), Q, k)
+    for i in range(len(Q)):
+        ri, rd = O.exhaustive_topk(X, Q[i], k)
+        np.testing.assert_array_equal(gt.ids[i], ri)
+        np.testing.assert_array_equal(gt.dists[i], rd)
+    # dataset rows as queries (exact_knn_rows: the build's consensus probe)
+    from paper_1912_01059_b200.search import exact_knn_rows
+
+    rows = rng.choice(X.shape[0], size=40, replace=False).astype(np.int32)
+    ids, dd = exact_knn_rows(ga.Dataset(X), rows, k)
+    for j, r in enumerate(rows):
+        ri, rd = O.exhaustive_topk(X, X[r], k)
+        np.testing.assert_array_equal(ids[j], ri)
+        np.testing.assert_array_equal(dd[j], rd)

@@ -28,5 +28,10 @@ for s in $stages; do
     long) free -g; nproc
           timeout 1800 python bench.py --workload deep10m --steps 10 --warmup 3 --no-ref-build --out gpurun_out/b_deep10m.json > gpurun_out/b_deep10m.log 2>&1; echo "deep10m rc=$?"; tail -c 300 gpurun_out/b_deep10m.log; echo
           timeout 3000 python bench.py --workload c5 --steps 10 --warmup 3 --out gpurun_out/b_c5.json > gpurun_out/b_c5.log 2>&1; echo "c5 rc=$?"; tail -c 300 gpurun_out/b_c5.log; echo ;;
+    c1) timeout 900 python bench.py --workload c1 --steps 10 --warmup 3 --out gpurun_out/b_c1.json > gpurun_out/b_c1.log 2>&1; echo "c1 rc=$?"
+        timeout 900 python bench.py --workload c1 --impl reference --steps 3 --warmup 1 --out gpurun_out/b_c1_ref.json > gpurun_out/b_c1_ref.log 2>&1; echo "c1 ref rc=$?"; tail -c 400 gpurun_out/b_c1_ref.log; echo ;;
+    ncuw) for w in sift1m-f32 gist1m; do
+            timeout 1500 ncu --set full --clock-control none --kernel-name-base mangled -k regex:_ZN4ggnn12query_kernelIffLi -s 6 -c 1 -f \
+              -o gpurun_out/query_$w python bench.py --workload $w --steps 2 --warmup 3 --tau 0.6 --no-cpu-baseline --no-ref-build > gpurun_out/ncu_$w.log 2>&1; echo "ncu $w rc=$?"; done ;;
   esac
 done
