@@ -302,6 +302,9 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
     per_node = layer.k_nn + (int(resc_id.shape[1]) if resc_id is not None else 0)
     ws.ensure_requests(max(4096, layer.node_count * per_node // 16), SYM_FALLBACK)
     lstruct = G.layer_struct(layer, d_max)
+    if TRACE is not None:
+        _sync()
+        t_check = time.perf_counter()
     while True:
         ws.req_count.zero_()
         N.call("ggnn_sym_check_layer", N.ctypes.byref(dv.struct), N.ctypes.byref(lstruct), N.ptr(dev["nnd"]),
@@ -312,6 +315,9 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
             break
         ws.ensure_requests(2 * cnt, SYM_FALLBACK)  # checks do not mutate the layer: rerun
     dropped = rounds = 0
+    if TRACE is not None:
+        _sync()
+        t_claim = time.perf_counter()
     if cnt:
         ws.stage[:cnt].zero_()
         ws.tgt[:cnt].fill_(-1)
@@ -337,8 +343,11 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
         layer._version += 1
         dropped = int(ws.dropped.item())
     if TRACE is not None:
+        _sync()
+        t_end = time.perf_counter()
         stage = ws.stage[:cnt].cpu().numpy() if cnt else np.zeros(0)
         TRACE.append({"layer": j, "nodes": layer.node_count, "pairs": layer.node_count * per_node, "requests": cnt,
+                      "check_s": t_claim - t_check, "claim_s": t_end - t_claim,
                       "claimed": int((stage == -1).sum()), "resolved": int((stage == -3).sum()), "dropped": dropped,
                       "rounds": rounds, "mean_sym": float(dev["symc"].double().mean().item())})
     return dropped
