@@ -106,7 +106,15 @@ int ggnn_sym_check_layer(const ggnn_vectors *X, const ggnn_layer *layer, const d
 int ggnn_sym_claim_round(const int32_t *d_req, int64_t nreq, int32_t n_fallback, int32_t *d_adj,
                          int32_t *d_sym_count, int32_t k, int32_t k_nn, int32_t *d_best_scratch, int32_t *d_stage,
                          int32_t *d_tgt_scratch, int32_t *d_dropped, int32_t *d_pending, int32_t x_end,
-                         int32_t *d_first_scratch, void *stream);
+                         int32_t *d_first_scratch, const int32_t *d_idx, void *stream);
+
+/* The still-open requests (d_stage[r] >= 0) among d_idx_in[0 .. n_in) (NULL:
+ * requests 0 .. n_in - 1) -> d_idx_out, their count -> *d_n_out.  Rounds late
+ * in a pass then touch only the requests that are still open (d_idx of
+ * ggnn_sym_claim_round / ggnn_sym_recheck, nreq = the count).  No reference
+ * counterpart (the reference walks its requests sequentially). */
+int ggnn_sym_compact(const int32_t *d_stage, const int32_t *d_idx_in, int64_t n_in, int32_t *d_idx_out,
+                     int32_t *d_n_out, void *stream);
 
 /* Re-check of open requests on the current graph (between claim rounds):
  * for every r with d_stage[r] >= 0, re-runs the reachability search of
@@ -115,7 +123,7 @@ int ggnn_sym_claim_round(const int32_t *d_req, int64_t nreq, int32_t n_fallback,
  * fallbacks in place.  Requests of nodes x >= x_end are skipped. */
 int ggnn_sym_recheck(const ggnn_vectors *X, const ggnn_layer *layer, int32_t *d_req, int64_t nreq, int32_t *d_stage,
                      int32_t x_end, double tau, double d_nn1_max, int32_t budget, int32_t k_out, int32_t prioq_size,
-                     int32_t visited_size, int32_t n_fallback, void *stream);
+                     int32_t visited_size, int32_t n_fallback, const int32_t *d_idx, void *stream);
 
 /* Replaces: compute_stats (build.py:275-280) / live_d_nn1_max
  * (graph.py:196-199): d_out[4] = {max of finite values (0 if none), sum of

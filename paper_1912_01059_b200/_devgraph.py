@@ -91,6 +91,7 @@ class Workspace:
         self.dropped = t.zeros((1,), dtype=t.int32, device=dev)
         self.reduced = t.zeros((1,), dtype=t.int32, device=dev)
         self.pending = t.zeros((1,), dtype=t.int32, device=dev)
+        self.n_open = t.zeros((1,), dtype=t.int32, device=dev)
 
     def ensure_requests(self, cap: int, n_fallback: int):
         if cap > self.req_cap:
@@ -100,6 +101,7 @@ class Workspace:
             self.req = t.empty((cap, 5 + n_fallback), dtype=t.int32, device=dev)
             self.stage = t.empty((cap,), dtype=t.int32, device=dev)
             self.tgt = t.empty((cap,), dtype=t.int32, device=dev)
+            self.open_idx = (t.empty((cap,), dtype=t.int32, device=dev), t.empty((cap,), dtype=t.int32, device=dev))
 
     def stats(self, values) -> tuple[float, float, int, int]:
         N.call("ggnn_layer_stats", N.ptr(values), values.numel(), N.ptr(self.stats_scratch), N.ptr(self.stats_out),

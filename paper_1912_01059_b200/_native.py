@@ -82,8 +82,9 @@ _SIGS = {
     "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_merge_rows_range": [I64, I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_sym_check_layer": [P, P, P, P, P, I32, F64, F64, I32, I32, I32, I32, I32, P, P, I64, P],
-    "ggnn_sym_claim_round": [P, I64, I32, P, P, I32, I32, P, P, P, P, P, I32, P, P],
-    "ggnn_sym_recheck": [P, P, P, I64, P, I32, F64, F64, I32, I32, I32, I32, I32, P],
+    "ggnn_sym_claim_round": [P, I64, I32, P, P, I32, I32, P, P, P, P, P, I32, P, P, P],
+    "ggnn_sym_compact": [P, P, I64, P, P, P],
+    "ggnn_sym_recheck": [P, P, P, I64, P, I32, F64, F64, I32, I32, I32, I32, I32, P, P],
     "ggnn_layer_stats": [P, I64, P, P, P],
     "ggnn_layer_stats_scratch_bytes": [],
     "ggnn_shard_block_bytes": [I64, I32],

@@ -29,6 +29,7 @@ SYM_CHECK_VISITED = 128
 SYM_FALLBACK = 8
 MAX_SLOTS = 32  # adjacency slots per node the kernels handle (ggnn_common.cuh MAX_K)
 CLAIM_CHECK = int(__import__("os").environ.get("GGNN_CLAIM_CHECK", "4"))  # claim rounds per pending read-back
+CLAIM_COMPACT = __import__("os").environ.get("GGNN_CLAIM_COMPACT", "1") != "0"  # rounds over the open requests only
 # node windows per symmetrize pass: requests of x-window w are re-checked after the
 # claims of windows < w, approximating the reference's sequential x order
 # Node windows per symmetrize / merge pass: the reference walks the nodes of a
@@ -324,22 +325,35 @@ def _symmetrize_dev(h, j: int, tau_build: float, resc=None) -> int:
         ws.dropped.zero_()
         nc = layer.node_count
         windows = max(1, min(_sym_windows(nc), cnt))
+        # the rounds' item list: all requests at first, then (at every
+        # read-back) only those still open -- most settle in the first rounds,
+        # and late rounds would otherwise scan every settled request again
+        idx, n_items, flip = None, cnt, 0
         while True:
             x_end = nc if rounds >= windows else (nc * (rounds + 1) + windows - 1) // windows
             if rounds:
-                N.call("ggnn_sym_recheck", N.ctypes.byref(dv.struct), N.ctypes.byref(lstruct), N.ptr(ws.req), cnt,
-                       N.ptr(ws.stage), x_end, float(tau_build), d_max, SYM_CHECK_BUDGET, k_out, prioq,
-                       SYM_CHECK_VISITED, SYM_FALLBACK, N.stream_ptr())
-            N.call("ggnn_sym_claim_round", N.ptr(ws.req), cnt, SYM_FALLBACK, N.ptr(dev["adj"]), N.ptr(dev["symc"]),
-                   layer.k, layer.k_nn, N.ptr(ws.best), N.ptr(ws.stage), N.ptr(ws.tgt), N.ptr(ws.dropped),
-                   N.ptr(ws.pending), x_end, N.ptr(ws.first), N.stream_ptr())
+                N.call("ggnn_sym_recheck", N.ctypes.byref(dv.struct), N.ctypes.byref(lstruct), N.ptr(ws.req),
+                       n_items, N.ptr(ws.stage), x_end, float(tau_build), d_max, SYM_CHECK_BUDGET, k_out, prioq,
+                       SYM_CHECK_VISITED, SYM_FALLBACK, N.ptr(idx), N.stream_ptr())
+            N.call("ggnn_sym_claim_round", N.ptr(ws.req), n_items, SYM_FALLBACK, N.ptr(dev["adj"]),
+                   N.ptr(dev["symc"]), layer.k, layer.k_nn, N.ptr(ws.best), N.ptr(ws.stage), N.ptr(ws.tgt),
+                   N.ptr(ws.dropped), N.ptr(ws.pending), x_end, N.ptr(ws.first), N.ptr(idx), N.stream_ptr())
             rounds += 1
             # the open-request count is read back (a host sync) only every
-            # CLAIM_CHECK rounds once every window is active: rounds after the
-            # last request settled are no-ops (every kernel skips settled
-            # requests), so the extra ones cost launches, not results
-            if x_end == nc and (rounds - windows) % CLAIM_CHECK == 0 and int(ws.pending.item()) == 0:
-                break
+            # CLAIM_CHECK rounds: rounds after the last request settled are
+            # no-ops (every kernel skips settled requests), so the extra ones
+            # cost launches, not results
+            if not CLAIM_COMPACT:
+                if x_end == nc and (rounds - windows) % CLAIM_CHECK == 0 and int(ws.pending.item()) == 0:
+                    break
+                continue
+            if (rounds - windows) % CLAIM_CHECK == 0 or (rounds < windows and rounds % (2 * CLAIM_CHECK) == 0):
+                out = ws.open_idx[flip]
+                N.call("ggnn_sym_compact", N.ptr(ws.stage), N.ptr(idx), n_items, N.ptr(out), N.ptr(ws.n_open),
+                       N.stream_ptr())
+                idx, n_items, flip = out, int(ws.n_open.item()), flip ^ 1
+                if x_end == nc and n_items == 0:
+                    break
         layer._version += 1
         dropped = int(ws.dropped.item())
     if TRACE is not None:

@@ -616,22 +616,28 @@ struct ClaimArgs {
   int32_t* pending;
   int32_t x_end;  // requests of nodes x >= x_end are not active yet
   int32_t* first; // (node_count), INT_MAX outside a round: lowest open pair index per x
+  const int32_t* idx;  // the requests of this round (nreq entries; nullptr: 0 .. nreq - 1)
 };
+
+__device__ __forceinline__ int64_t claim_item(const ClaimArgs& a, int64_t i) { return a.idx ? (int64_t)a.idx[i] : i; }
 
 // Requests that share x are serialised too: once one neighbour z of x links
 // back to x, x's other neighbours usually reach x through z (the reference
 // resolves ~90% of snapshot verdict-2 pairs this way), so only the lowest
 // open pair index of every x proposes in a round.
 __global__ void claim_first_kernel(const __grid_constant__ ClaimArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.nreq || a.stage[r] < 0) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nreq) return;
+  const int64_t r = claim_item(a, i);
+  if (a.stage[r] < 0) return;
   const int32_t* q = a.req + r * (REQ_HDR + a.n_fallback);
   if (q[1] < a.x_end) atomicMin(a.first + q[1], q[0]);
 }
 
 __global__ void claim_propose_kernel(const __grid_constant__ ClaimArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.nreq) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nreq) return;
+  const int64_t r = claim_item(a, i);
   int s = a.stage[r];
   if (s < 0) return;
   const int32_t* q = a.req + r * (REQ_HDR + a.n_fallback);
@@ -662,8 +668,9 @@ __global__ void claim_propose_kernel(const __grid_constant__ ClaimArgs a) {
 }
 
 __global__ void claim_accept_kernel(const __grid_constant__ ClaimArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.nreq) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nreq) return;
+  const int64_t r = claim_item(a, i);
   const int t = a.tgt[r];
   if (t < 0) return;
   const int32_t* q = a.req + r * (REQ_HDR + a.n_fallback);
@@ -676,9 +683,10 @@ __global__ void claim_accept_kernel(const __grid_constant__ ClaimArgs a) {
 }
 
 __global__ void claim_reset_kernel(const __grid_constant__ ClaimArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int open = 0;
-  if (r < a.nreq) {
+  if (i < a.nreq) {
+    const int64_t r = claim_item(a, i);
     const int t = a.tgt[r];
     if (t >= 0) {
       a.best[t] = INT_MAX;
@@ -690,6 +698,25 @@ __global__ void claim_reset_kernel(const __grid_constant__ ClaimArgs a) {
   }
   const unsigned m = __ballot_sync(FULL, open);
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(a.pending, __popc(m));
+}
+
+// The open requests (stage >= 0) of a list, in list order (warp-aggregated
+// slots, so the order is deterministic within a warp but not across warps;
+// the claim kernels do not depend on the order of their items).
+__global__ void compact_open_kernel(const int32_t* stage, const int32_t* idx_in, int64_t n_in, int32_t* idx_out,
+                                    int32_t* n_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  int32_t r = 0;
+  if (i < n_in) {
+    r = idx_in ? idx_in[i] : (int32_t)i;
+    keep = stage[r] >= 0;
+  }
+  const unsigned m = __ballot_sync(FULL, keep);
+  int base = 0;
+  if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(n_out, __popc(m));
+  base = __shfl_sync(FULL, base, 0);
+  if (keep) idx_out[base + __popc(m & lanemask_lt())] = r;
 }
 
 // ------------------------------------------------------------ layer stats
@@ -878,12 +905,15 @@ int ggnn_merge_rows_range(int64_t node_begin, int64_t count, int32_t k, int32_t 
 int ggnn_sym_claim_round(const int32_t* d_req, int64_t nreq, int32_t n_fallback, int32_t* d_adj,
                          int32_t* d_sym_count, int32_t k, int32_t k_nn, int32_t* d_best_scratch, int32_t* d_stage,
                          int32_t* d_tgt_scratch, int32_t* d_dropped, int32_t* d_pending, int32_t x_end,
-                         int32_t* d_first_scratch, void* stream) {
+                         int32_t* d_first_scratch, const int32_t* d_idx, void* stream) {
   GGNN_CHECK_ARG(d_req && d_adj && d_sym_count && d_best_scratch && d_stage && d_tgt_scratch && d_dropped &&
                  d_pending && d_first_scratch, "invalid arguments");
-  if (nreq <= 0) return GGNN_OK;
+  if (nreq <= 0) {
+    GGNN_CUDA_TRY(cudaMemsetAsync(d_pending, 0, sizeof(int32_t), as_stream(stream)));
+    return GGNN_OK;
+  }
   ClaimArgs a{d_req, nreq, n_fallback, d_adj, d_sym_count, k, k_nn, d_best_scratch, d_stage, d_tgt_scratch,
-              d_dropped, d_pending, x_end, d_first_scratch};
+              d_dropped, d_pending, x_end, d_first_scratch, d_idx};
   cudaStream_t st = as_stream(stream);
   const unsigned grid = (unsigned)((nreq + 255) / 256);
   claim_first_kernel<<<grid, 256, 0, st>>>(a);
@@ -891,6 +921,17 @@ int ggnn_sym_claim_round(const int32_t* d_req, int64_t nreq, int32_t n_fallback,
   claim_accept_kernel<<<grid, 256, 0, st>>>(a);
   GGNN_CUDA_TRY(cudaMemsetAsync(d_pending, 0, sizeof(int32_t), st));
   claim_reset_kernel<<<grid, 256, 0, st>>>(a);
+  GGNN_LAUNCH_CHECK();
+  return GGNN_OK;
+}
+
+int ggnn_sym_compact(const int32_t* d_stage, const int32_t* d_idx_in, int64_t n_in, int32_t* d_idx_out,
+                     int32_t* d_n_out, void* stream) {
+  GGNN_CHECK_ARG(d_stage && d_idx_out && d_n_out && n_in >= 0, "invalid arguments");
+  cudaStream_t st = as_stream(stream);
+  GGNN_CUDA_TRY(cudaMemsetAsync(d_n_out, 0, sizeof(int32_t), st));
+  if (n_in == 0) return GGNN_OK;
+  compact_open_kernel<<<(unsigned)((n_in + 255) / 256), 256, 0, st>>>(d_stage, d_idx_in, n_in, d_idx_out, d_n_out);
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }

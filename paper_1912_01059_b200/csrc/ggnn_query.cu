@@ -563,6 +563,7 @@ struct SymArgs {
   bool recheck;
   int32_t* stage;
   int32_t x_end;  // recheck only requests of nodes x < x_end
+  const int32_t* idx;  // recheck: the request of item i is idx[i] (nullptr: i)
   int* work;      // persistent-warp item counter (nullptr: one item per warp)
   unsigned long long* acc;  // build accounting (visited, steps) or nullptr
 };
@@ -576,6 +577,7 @@ __device__ __forceinline__ void symcheck_kernel_one(const SymArgs& a, uint8_t* s
   double dxz;
   int32_t* rec = nullptr;
   if (a.recheck) {
+    if (a.idx) pi = a.idx[pi];
     if (a.stage[pi] < 0) return;
     rec = a.req + pi * rstride;
     x = rec[1];
@@ -1369,7 +1371,8 @@ int ggnn_sym_check_layer(const ggnn_vectors* X, const ggnn_layer* layer, const d
 
 int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_req, int64_t nreq,
                       int32_t* d_stage, int32_t x_end, double tau, double d_nn1_max, int32_t budget, int32_t k_out,
-                      int32_t prioq_size, int32_t visited_size, int32_t n_fallback, void* stream) {
+                      int32_t prioq_size, int32_t visited_size, int32_t n_fallback, const int32_t* d_idx,
+                      void* stream) {
   GGNN_CHECK_ARG(X && X->d_data && layer && layer->d_adj && d_req && d_stage, "invalid arguments");
   GGNN_CHECK_ARG(layer->k >= 1 && layer->k <= MAX_K, "invalid layer geometry");
   GGNN_CHECK_ARG(k_out >= 1 && k_out <= 32 && n_fallback >= 0 && n_fallback <= 32, "k_out / n_fallback in [1, 32]");
@@ -1390,6 +1393,7 @@ int ggnn_sym_recheck(const ggnn_vectors* X, const ggnn_layer* layer, int32_t* d_
   a.recheck = true;
   a.stage = d_stage;
   a.x_end = x_end;
+  a.idx = d_idx;
   int keysize = X->dtype == GGNN_U8 ? 4 : 8;
   a.region = set_layout(a.c, X->d, qelem_of(X->dtype), keysize);
   cudaStream_t st = as_stream(stream);
