@@ -143,6 +143,7 @@ struct SearchArgs {
   int seg_div;
   int seg_size;
   int* work;  // persistent-warp item counter (nullptr: one item per warp)
+  int chunk;  // items claimed per counter update
   // fused sharded exchange (ggnn_query_batch_push): block `push_rank` of
   // parity half `push_parity` of every receive allocation
   uint8_t* push_peers[GGNN_P2P_MAX_RANKS];
@@ -161,20 +162,37 @@ struct SearchArgs {
 };
 
 // Persistent warps: with a work counter (zeroed before the launch) every warp
-// takes the next item when it finishes one, so uneven search lengths never
+// takes the next items when it finishes one, so uneven search lengths never
 // leave a warp idle until its CTA-mates finish; without one each warp runs
-// its static item (one item per warp, grid covering all items).
-__device__ __forceinline__ int64_t first_item(int* work) {
-  if (!work) return (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// its static item (one item per warp, grid covering all items).  Items are
+// claimed WORK_CHUNK at a time: one atomic per item on a single counter cost
+// more than the item itself for the many instant ones of a symmetrize pass
+// (a pair already linked back, a request settled in an earlier round).
+// The chunk shrinks to 1 when there are few items per resident warp (a late
+// claim round's handful of re-checks must still spread over all SMs).
+#ifndef GGNN_WORK_CHUNK
+#define GGNN_WORK_CHUNK 8
+#endif
+struct WorkCursor {
+  int64_t cur, end;
+  int chunk;
+};
+__device__ __forceinline__ int64_t grab_chunk(int* work, WorkCursor& w) {
   int v = 0;
-  if (lane_id() == 0) v = atomicAdd(work, 1);
-  return (int64_t)__shfl_sync(FULL, v, 0);
+  if (lane_id() == 0) v = atomicAdd(work, w.chunk);
+  w.cur = (int64_t)__shfl_sync(FULL, v, 0);
+  w.end = w.cur + w.chunk;
+  return w.cur;
 }
-__device__ __forceinline__ int64_t next_item(int* work) {
+__device__ __forceinline__ int64_t first_item(int* work, int chunk, WorkCursor& w) {
+  if (!work) return (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  w.chunk = chunk;
+  return grab_chunk(work, w);
+}
+__device__ __forceinline__ int64_t next_item(int* work, WorkCursor& w) {
   if (!work) return INT64_MAX;
-  int v = 0;
-  if (lane_id() == 0) v = atomicAdd(work, 1);
-  return (int64_t)__shfl_sync(FULL, v, 0);
+  if (++w.cur < w.end) return w.cur;
+  return grab_chunk(work, w);
 }
 
 // Staged queries: wait (bounded, ~50 ms) until the host's copy stream has
@@ -355,7 +373,8 @@ __global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeo
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
   if constexpr (GGNN_PERSISTENT != 0) {
-    for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
+    WorkCursor wc;
+    for (int64_t qi = first_item(a.work, a.chunk, wc); qi < a.m; qi = next_item(a.work, wc))
       query_kernel_one<TX, TQ, LP, PUSH, STAGED>(a, smem_w, vring_lane, qi);
   } else {
     const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -396,7 +415,8 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kern
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
   if constexpr (GGNN_PERSISTENT != 0) {
-    for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
+    WorkCursor wc;
+    for (int64_t qi = first_item(a.work, a.chunk, wc); qi < a.m; qi = next_item(a.work, wc))
       greedy_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
   } else {
     const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -518,7 +538,8 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_ker
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
   if constexpr (GGNN_PERSISTENT != 0) {
-    for (int64_t qi = first_item(a.work); qi < a.m; qi = next_item(a.work))
+    WorkCursor wc;
+    for (int64_t qi = first_item(a.work, a.chunk, wc); qi < a.m; qi = next_item(a.work, wc))
       descent_kernel_one<TX, TQ, LP>(a, smem_w, vring_lane, qi);
   } else {
     const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -565,6 +586,7 @@ struct SymArgs {
   int32_t x_end;  // recheck only requests of nodes x < x_end
   const int32_t* idx;  // recheck: the request of item i is idx[i] (nullptr: i)
   int* work;      // persistent-warp item counter (nullptr: one item per warp)
+  int chunk;      // items claimed per counter update
   unsigned long long* acc;  // build accounting (visited, steps) or nullptr
 };
 
@@ -678,7 +700,8 @@ __global__ void __launch_bounds__(SYM_THREADS, SYM_MIN_BLOCKS) symcheck_kernel(c
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
   if constexpr (GGNN_SYM_PERSISTENT != 0) {
-    for (int64_t pi = first_item(a.work); pi < a.npairs; pi = next_item(a.work))
+    WorkCursor wc;
+    for (int64_t pi = first_item(a.work, a.chunk, wc); pi < a.npairs; pi = next_item(a.work, wc))
       symcheck_kernel_one<TX, LP>(a, smem_w, vring_lane, pi);
   } else {
     const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -864,7 +887,11 @@ int launch_items(Kern kern, Args a, int64_t items, size_t region, cudaStream_t s
   GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t grid = (items + W - 1) / W;
   a.work = persistent ? work_counter(st) : nullptr;
-  if (a.work) grid = persistent_grid(kern, W * 32, smem, grid);
+  a.chunk = 1;
+  if (a.work) {
+    grid = persistent_grid(kern, W * 32, smem, grid);
+    a.chunk = (int)std::max<int64_t>(1, std::min<int64_t>(GGNN_WORK_CHUNK, items / (grid * W * 16)));
+  }
   kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;

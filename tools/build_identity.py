@@ -25,3 +25,10 @@ for flag in (True, False, True):
 same = all(np.array_equal(a.adjacency, b.adjacency) and np.array_equal(a.sym_count, b.sym_count)
            for a, b in zip(out[True].layers, out[False].layers))
 print("identical graphs:", same)
+import hashlib  # noqa: E402
+
+hsh = hashlib.sha256()
+for L in out[True].layers:
+    hsh.update(L.adjacency.tobytes())
+    hsh.update(L.sym_count.tobytes())
+print("graph sha256:", hsh.hexdigest()[:16])
