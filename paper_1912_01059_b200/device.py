@@ -78,19 +78,21 @@ class DeviceVectors:
 
     def queries(self, Q: np.ndarray):
         """Upload a (m, d) float32 query table; integral queries against a
-        uint8 table travel as uint8 (exact integer distances)."""
+        uint8 table are searched as uint8 (exact integer distances).  The
+        check and the narrowing run on the device (ggnn_f32_to_u8): one
+        float upload instead of a host-side scan of every value."""
         Q = np.ascontiguousarray(Q, dtype=np.float32)
         if Q.ndim != 2 or Q.shape[1] != self.d:
             raise ValueError(f"query shape {Q.shape} does not match index dimension {self.d}")
-        if self.dtype == N.GGNN_U8 and Q.size and _is_u8_exact(Q):
-            dq = N.to_dev(Q.astype(np.uint8))
-            return dq, N.queries_struct(data=dq, dtype_code=N.GGNN_U8)
         dq = N.to_dev(Q)
+        if self.dtype == N.GGNN_U8 and Q.size:
+            t = N.torch()
+            u8 = t.empty(Q.shape, dtype=t.uint8, device=dq.device)
+            flag = t.ones(1, dtype=t.int32, device=dq.device)
+            N.call("ggnn_f32_to_u8", N.ptr(dq), Q.size, N.ptr(u8), N.ptr(flag), N.stream_ptr())
+            if int(flag.item()) == 1:
+                return u8, N.queries_struct(data=u8, dtype_code=N.GGNN_U8)
         return dq, N.queries_struct(data=dq, dtype_code=N.GGNN_F32)
-
-
-def _is_u8_exact(Q: np.ndarray) -> bool:
-    return bool(((Q >= 0) & (Q <= 255) & (Q == np.rint(Q))).all())
 
 
 class DeviceLayer:
