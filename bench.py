@@ -476,9 +476,6 @@ def run_index(args, dist, torch):
     rank, G = dist.rank, dist.world
     m = args.queries
     base = make_base(args)
-    ref_build = None
-    if rank == 0 and G == 1 and not args.no_ref_build:  # the reference's CPU build of a 10k subsample, meanwhile
-        ref_build = start_reference_build(base[:10_000])
     B = max(1, min(args.batches, args.steps))
     batches = [make_queries(args, rank * B + b) for b in range(B)]
     Q = batches[0]
@@ -603,8 +600,6 @@ def run_index(args, dist, torch):
         if (ROOT / "oracle" / "_ref" / "graphann_ref").exists():
             import shutil
 
-            ref_build_res = finish_reference_build(ref_build)  # before the query pool takes every core
-            ref_build = None
             root = export_index(h, base, Q, {"tau": tau})
             try:
                 pool = RefPool(root, m)
@@ -619,8 +614,10 @@ def run_index(args, dist, torch):
         else:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": "oracle/_ref not built on this box"}
-    if ref_build is not None:
-        ref_build_res = finish_reference_build(ref_build)
+    if rank == 0 and G == 1 and not args.no_ref_build:
+        # the reference's CPU build of a 10k subsample, after every timed
+        # section (it runs on one host core in a process of its own)
+        ref_build_res = finish_reference_build(start_reference_build(base[:10_000]))
     ref_build_info = None
     if ref_build_res is not None:
         sub = ga.Dataset(np.ascontiguousarray(base[:10_000]))
@@ -738,6 +735,8 @@ def run_sharded(args, dist, torch):
     params = [_params(qcfg, _qflags(dh, False)) for dh in dhs]
     stream = torch.cuda.current_stream()
     qev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    if args.exchange == "p2p" and G > 1 and S != 1:
+        raise SystemExit("--exchange p2p needs one shard per rank (the fused exchange pushes one block per rank)")
     x = grp.p2p(m, 10) if (args.exchange == "p2p" and G > 1) else None
 
     def step(i, timed=False):
