@@ -107,11 +107,11 @@ def workload_desc(args) -> str:
     return WORKLOADS[args.workload][3].format(n=args.n, d=args.d)
 
 
-def config_of(args, tau) -> dict:
+def config_of(args, tau, prioq=256, visited=512, max_it=1000) -> dict:
     """The `config` object of the JSON line -- identical in both arms."""
     return {"workload": f"{args.workload}: {workload_desc(args)}", "queries_per_step": args.queries, "k": 10,
-            "k_build": 24, "tau": tau, "recall_target": f"R@10>={args.target}",
-            "queries": "a fresh seeded batch every step"}
+            "k_build": 24, "tau": tau, "prioq_size": prioq, "visited_size": visited, "max_iterations": max_it,
+            "recall_target": f"R@10>={args.target}", "queries": "a fresh seeded batch every step"}
 
 
 # ------------------------------------------------------------------ data
@@ -179,17 +179,60 @@ def k_recall_at(ids, gt, k):
     return float(np.mean([len(set(ids[i, :k].tolist()) & set(gt[i, :k].tolist())) / k for i in range(len(ids))]))
 
 
+# the reference's QueryConfig cache (prioq_size, visited_size) first; larger
+# ones only when no tau reaches the target with it (C4: the searches end on
+# an empty queue, not on the stopping rule, so tau alone cannot get there)
+CACHES = [(256, 512), (512, 1024), (1024, 2048), (2048, 4096)]
+CACHE_TAUS = [0.6, 1.0, 1.5, 2.0]
+
+
+def qconfig(row, ga):
+    return ga.QueryConfig(k_out=10, tau=row["tau"], prioq_size=row["prioq_size"], visited_size=row["visited_size"],
+                          max_iterations=max(1000, 2 * row["prioq_size"]))
+
+
 def choose_tau(query_fn, gt_ids, fixed, target):
-    """Smallest tau of the sweep with R@10 >= target; (row, sweep, reached)."""
+    """Smallest tau with R@10 >= target: the coarse sweep TAUS, then steps of
+    0.01 between the last tau below the target and the first one above it
+    ("finer steps near the R@10 = 0.99 crossing"); if the default
+    cache never gets there, the next larger cache of CACHES.
+    query_fn(tau, prioq, visited) -> (ids, counters).  Returns (row, sweep,
+    reached); row carries tau, prioq_size and visited_size."""
     sweep = []
-    for tau in ([fixed] if fixed is not None else TAUS):
-        ids, cnt = query_fn(tau)
-        row = {"tau": tau, "R@1": recall_at(ids, gt_ids[:, 0], 1), "R@10": recall_at(ids, gt_ids[:, 0], 10),
-               "kR@10": k_recall_at(ids, gt_ids, 10), "V": float(cnt[:, 0].mean()), "T": float(cnt[:, 1].mean())}
+
+    def run(tau, pq, vs):
+        ids, cnt = query_fn(tau, pq, vs)
+        row = {"tau": tau, "prioq_size": pq, "visited_size": vs, "R@1": recall_at(ids, gt_ids[:, 0], 1),
+               "R@10": recall_at(ids, gt_ids[:, 0], 10), "kR@10": k_recall_at(ids, gt_ids, 10),
+               "V": float(cnt[:, 0].mean()), "T": float(cnt[:, 1].mean())}
         sweep.append(row)
-        if row["R@10"] >= target:
-            return row, sweep, True
-    return sweep[-1], sweep, False
+        return row
+
+    for ci, (pq, vs) in enumerate(CACHES if fixed is None else CACHES[:1]):
+        prev = None
+        for tau in ([fixed] if fixed is not None else (TAUS if ci == 0 else CACHE_TAUS)):
+            row = run(tau, pq, vs)
+            if row["R@10"] >= target:
+                if prev is not None:
+                    for k in range(1, int(round((tau - prev) * 100))):
+                        fine = run(round(prev + 0.01 * k, 2), pq, vs)
+                        if fine["R@10"] >= target:
+                            return fine, sweep, True
+                return row, sweep, True
+            prev = tau
+    best = max(sweep, key=lambda r: r["R@10"])
+    return best, sweep, False
+
+
+def recall_queries(args, batches):
+    """The queries tau is chosen on (both arms): every query of every timed
+    batch for the uint8 workloads (exact ground truth on the tensor cores is
+    cheap), a subsample of batch 0 for the float ones."""
+    m = batches[0].shape[0]
+    if args.workload in ("c1", "sift1m"):
+        gt_m = min(args.gt_queries or m, m)
+        return np.ascontiguousarray(np.concatenate([b_[:gt_m] for b_ in batches]))
+    return np.ascontiguousarray(batches[0][:min(args.gt_queries or 1000, m)])
 
 
 # ---------------------------------------------------------------- clocks
@@ -350,7 +393,9 @@ def _ref_run(job):
     R, h, meta, Q = _REF
     q = np.ascontiguousarray(Q[lo:hi])
     t0 = time.perf_counter()
-    res = R.batch_query(h, q, R.QueryConfig(k_out=10, tau=meta["tau"]), threads=1)
+    res = R.batch_query(h, q, R.QueryConfig(k_out=10, tau=meta["tau"], prioq_size=meta["prioq_size"],
+                                            visited_size=meta["visited_size"],
+                                            max_iterations=meta["max_iterations"]), threads=1)
     dt = time.perf_counter() - t0
     ids = np.stack([np.pad(r.ids, (0, 10 - len(r.ids)), constant_values=-1) for r in res])
     return dt, ids
@@ -487,17 +532,19 @@ def run_index(args, dist, torch):
     # ---- recall: same-run exact ground truth on batch 0 -----------------
     torch.cuda.synchronize()
     t_gt = time.perf_counter()
-    gt_m = min(args.gt_queries or (m if args.workload in ("c1", "sift1m") else 1000), m)
-    gt_ids, _ = ga.search.exact_knn(ds, Q[:gt_m], 10)
+    # tau is chosen on the canonical batches 0 .. B-1 on every rank (replicas
+    # then all run the same tau; rank r > 0 times its own batches r*B ...)
+    QG = recall_queries(args, batches if rank == 0 else [make_queries(args, b) for b in range(B)])
+    gt_ids, _ = ga.search.exact_knn(ds, QG, 10)
     gt_s = time.perf_counter() - t_gt
 
-    def qfn(tau):
-        r = ga.query_arrays(h, Q[:gt_m], ga.QueryConfig(k_out=10, tau=tau))
+    def qfn(tau, pq, vs):
+        r = ga.query_arrays(h, QG, qconfig({"tau": tau, "prioq_size": pq, "visited_size": vs}, ga))
         return r.ids, r.counters
 
     chosen, sweep, reached = choose_tau(qfn, gt_ids, args.tau, args.target)
     tau = chosen["tau"]
-    qcfg = ga.QueryConfig(k_out=10, tau=tau)
+    qcfg = qconfig(chosen, ga)
 
     # ---- device-resident kernel timing (value) ---------------------------
     dh = device_hierarchy(h)
@@ -600,7 +647,9 @@ def run_index(args, dist, torch):
         if (ROOT / "oracle" / "_ref" / "graphann_ref").exists():
             import shutil
 
-            root = export_index(h, base, Q, {"tau": tau})
+            root = export_index(h, base, Q, {"tau": tau, "prioq_size": qcfg.prioq_size,
+                                             "visited_size": qcfg.visited_size,
+                                             "max_iterations": qcfg.max_iterations})
             try:
                 pool = RefPool(root, m)
                 try:
@@ -634,7 +683,7 @@ def run_index(args, dist, torch):
         "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8" if dv.exact_integers else "f32",
         "data": f"synthetic, seed 1234: {workload_desc(args)}; {B} distinct query batches of {m}",
-        "config": config_of(args, tau),
+        "config": config_of(args, tau, qcfg.prioq_size, qcfg.visited_size, qcfg.max_iterations),
         "build_seconds": build_s,
         "e2e": e2e,
         "gpu_launches": args.steps,
@@ -646,7 +695,7 @@ def run_index(args, dist, torch):
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "details": {
-            "recall_queries": gt_m, "recall": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
+            "recall_queries": int(QG.shape[0]), "recall": {k: chosen[k] for k in ("R@1", "R@10", "kR@10")},
             "recall_target_reached": reached, "mean_visited": chosen["V"], "mean_steps": chosen["T"],
             "tau_sweep": sweep, "ground_truth_seconds": gt_s,
             "build_note": f"warm process: a {warm_n}-point build ran first ({warm_s:.2f} s, module loading and "
@@ -716,13 +765,13 @@ def run_sharded(args, dist, torch):
     gt_m = min(args.gt_queries or 1000, m)
     gt_ids, _ = grp.exact_arrays(Q[:gt_m], 10)
 
-    def qfn(tau):
-        r = grp.query_arrays(Q[:gt_m], ga.QueryConfig(k_out=10, tau=tau))
+    def qfn(tau, pq, vs):
+        r = grp.query_arrays(Q[:gt_m], qconfig({"tau": tau, "prioq_size": pq, "visited_size": vs}, ga))
         return r.ids, r.counters
 
     chosen, sweep, reached = choose_tau(qfn, gt_ids, args.tau, args.target)
     tau = chosen["tau"]
-    qcfg = ga.QueryConfig(k_out=10, tau=tau)
+    qcfg = qconfig(chosen, ga)
 
     dhs = [device_hierarchy(h) for h, _ in grp.shards]
     dqs = [[dh.vectors.queries(b_) for dh in dhs] for b_ in batches]
@@ -818,7 +867,7 @@ def run_sharded(args, dist, torch):
         "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8" if e == 1 else "f32",
         "data": f"synthetic, seed 1234: {workload_desc(args)}; {B} distinct query batches of {m} (replicated)",
-        "config": config_of(args, tau),
+        "config": config_of(args, tau, qcfg.prioq_size, qcfg.visited_size, qcfg.max_iterations),
         "build_seconds": build_s,
         "e2e": {"value": m * args.steps / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(pinned[0].nbytes),
                 "d2h_bytes_per_step": int(out.ids.nbytes + out.dists.nbytes + out.counters.nbytes),
@@ -865,21 +914,25 @@ def prep_reference(args, torch):
 
     root = Path(args.prep_reference)
     base = make_base(args)
-    Q = make_queries(args, 0)
+    B = max(1, min(args.batches, args.steps))
+    batches = [make_queries(args, b) for b in range(B)]  # the GPU arm's (rank 0's) batches
+    Q = batches[0]
     h, _, _, _ = build_index(ga, base, torch)
-    m = Q.shape[0]
-    gt_m = min(args.gt_queries or (m if args.workload in ("c1", "sift1m") else 1000), m)
-    gt_ids, _ = ga.search.exact_knn(h.dataset, Q[:gt_m], 10)
+    QG = recall_queries(args, batches)
+    gt_ids, _ = ga.search.exact_knn(h.dataset, QG, 10)
 
-    def qfn(tau):
-        r = ga.query_arrays(h, Q[:gt_m], ga.QueryConfig(k_out=10, tau=tau))
+    def qfn(tau, pq, vs):
+        r = ga.query_arrays(h, QG, qconfig({"tau": tau, "prioq_size": pq, "visited_size": vs}, ga))
         return r.ids, r.counters
 
     chosen, sweep, reached = choose_tau(qfn, gt_ids, args.tau, args.target)
+    qc = qconfig(chosen, ga)
     ga.save_index(h, root / "index.ggnn")
     np.save(root / "base.npy", np.ascontiguousarray(base, dtype=np.float32))
     np.save(root / "queries.npy", np.ascontiguousarray(Q, dtype=np.float32))
-    (root / "meta.json").write_text(json.dumps({"tau": chosen["tau"], "reached": reached,
+    (root / "meta.json").write_text(json.dumps({"tau": chosen["tau"], "prioq_size": qc.prioq_size,
+                                                "visited_size": qc.visited_size,
+                                                "max_iterations": qc.max_iterations, "reached": reached,
                                                 "recall_gpu_same_tau": {k: chosen[k] for k in
                                                                         ("R@1", "R@10", "kR@10")}}))
 
@@ -906,7 +959,8 @@ def run_reference(args):
     root = Path(tempfile.mkdtemp(prefix="ggnn_ref_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None))
     try:
         cmd = [sys.executable, str(ROOT / "bench.py"), "--prep-reference", str(root), "--workload", args.workload,
-               "--points", str(args.n), "--dim", str(args.d), "--queries", str(args.queries)]
+               "--points", str(args.n), "--dim", str(args.d), "--queries", str(args.queries), "--steps",
+               str(args.steps), "--batches", str(args.batches)]
         if args.tau is not None:
             cmd += ["--tau", str(args.tau)]
         if args.gt_queries is not None:
@@ -946,7 +1000,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.queries / value * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic, seed 1234: {workload_desc(args)}",
-        "config": config_of(args, tau),
+        "config": config_of(args, tau, meta["prioq_size"], meta["visited_size"], meta["max_iterations"]),
         "build_seconds": (build_info or {}).get("reference_cpu_seconds") if args.workload == "c1" else None,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
                          "sample": info["sample"]},
