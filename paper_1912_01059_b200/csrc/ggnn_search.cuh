@@ -348,7 +348,30 @@ struct WarpSearch {
     // placed below o}.  Every source index is <= its destination and chunks
     // go downwards, so nothing is overwritten before it is read.
     const int p0 = __shfl_sync(FULL, p, 0);
-    for (int hi = newL; hi > p0; hi -= 32) {
+    // chunks wholly above the last candidate's slot only move up by madm
+    // (every candidate lies below them): a plain copy, no candidate masks
+    const int pl = __shfl_sync(FULL, p, madm - 1);  // admitted lanes are the prefix [0, madm)
+    int hi = newL;
+    for (; hi - 32 > pl; hi -= 32) {
+      const int o = hi - 32 + lane;
+      if constexpr (PACK) {
+        const uint64_t ee = re[o - madm];
+        const uint8_t vv = rvis[o - madm];
+        __syncwarp();
+        re[o] = ee;
+        rvis[o] = vv;
+      } else {
+        const Key kk = rk[o - madm];
+        const int ii = rid[o - madm];
+        const uint8_t vv = rvis[o - madm];
+        __syncwarp();
+        rk[o] = kk;
+        rid[o] = ii;
+        rvis[o] = vv;
+      }
+      __syncwarp();
+    }
+    for (; hi > p0; hi -= 32) {
       const int cb = hi - 32;
       const int o = cb + lane;
       const bool act = o >= p0;
