@@ -127,8 +127,8 @@ def make_base(args, n=None):
         return make_latent16(n=n, d=args.d, m=1, seed=1234)[0]
     if w in ("sift1m-f32", "gist1m"):
         return make_latent16(n=n, d=args.d, m=1, seed=1234, as_float=True)[0]
-    if w == "deep10m":
-        return make_deep_like(n, 1, d=args.d)[0]
+    if w == "deep10m":  # one draw with the held-out query rows (the generator's stream depends on its length)
+        return make_deep_like(n, args.queries, d=args.d)[0]
     raise ValueError(w)
 
 

@@ -185,7 +185,13 @@ int ggnn_sym_check_batch(const ggnn_vectors *X, const ggnn_layer *layer, const i
                          int32_t *d_verdict, int32_t *d_fallback, void *stream);
 
 /* Replaces: exhaustive_topk (_core.pyx:86-104), batched over queries, over
- * rows d_rows[0..nrows) of X (NULL = all rows), k <= 32; ties by row index. */
+ * rows d_rows[0..nrows) of X (NULL = all rows), any k >= 1; ties by row
+ * index; distances are the reference's sequential FP64 _sqdist values.
+ * Whole-table scans of at least 4096 rows run on the tensor cores: uint8
+ * tables as exact kind::i8, float tables (d % 8 == 0, k <= 32) as 3xTF32
+ * with a rigorous error bound and an exact re-score of every candidate.
+ * The float tensor-core path synchronizes the stream once (to send the rare
+ * query whose candidate list may be cut to the CUDA-core scan). */
 int ggnn_exhaustive_topk(const ggnn_vectors *X, const int32_t *d_rows, int64_t nrows, const ggnn_queries *Q,
                          int32_t k, int32_t *d_ids, double *d_dists, void *stream);
 

@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(128, 1) bf_tf32_kernel(const __grid_constant__
 // candidate limit, sequential FP64 re-score of the candidates, top-k by
 // (distance, row).  flag[q] = 1 when a list may have cut a candidate.
 __global__ void __launch_bounds__(256) bf_tf32_finalize(const Tf32Args a, const float* Qf, const double* qn_all,
-                                                       double xmax, int k, int32_t* out_ids, double* out_d,
-                                                       int32_t* flag, int32_t* nflag) {
+                                                       const unsigned long long* xmax_bits, int k, int32_t* out_ids,
+                                                       double* out_d, int32_t* flag, int32_t* nflag) {
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= a.m) return;
   const int lane = lane_id();
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) bf_tf32_finalize(const Tf32Args a, const 
   }
   const double ak = KO::shfl(bk, k - 1);
   const double qn = qn_all[q];
-  const double nrm = sqrt(qn) + sqrt(xmax);
+  const double nrm = sqrt(qn) + sqrt(__longlong_as_double((long long)*xmax_bits));
   const double lim = ak + 2.0 * (8.0 * a.d * 0x1p-23 + 0x1p-18) * nrm * nrm;
   // a full split list whose last key is within the limit may have dropped one
   bool unsafe = false;
@@ -407,14 +407,10 @@ int bf_topk_tf32(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d
   GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   bf_tf32_kernel<<<(unsigned)(qtiles * splits), TB_M, smem, st>>>(a);
   GGNN_LAUNCH_CHECK();
-  // the largest |x'|^2 is needed on the host side of the finalize launch
-  unsigned long long xm_bits = 0;
-  GGNN_CUDA_TRY(cudaMemcpyAsync(&xm_bits, xmax, 8, cudaMemcpyDeviceToHost, st));
-  GGNN_CUDA_TRY(cudaStreamSynchronize(st));
-  double xm;
-  memcpy(&xm, &xm_bits, 8);
-  bf_tf32_finalize<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(a, Qf, qn, xm, k, d_ids, d_dists, flag, nflag);
+  bf_tf32_finalize<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(a, Qf, qn, xmax, k, d_ids, d_dists, flag, nflag);
   GGNN_LAUNCH_CHECK();
+  // the one host synchronisation of this path: how many queries need the
+  // CUDA-core scan (almost always none)
   int32_t nf = 0;
   GGNN_CUDA_TRY(cudaMemcpyAsync(&nf, nflag, 4, cudaMemcpyDeviceToHost, st));
   GGNN_CUDA_TRY(cudaStreamSynchronize(st));

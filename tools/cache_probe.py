@@ -11,8 +11,8 @@ from paper_1912_01059_b200.synthetic import make_latent16  # noqa: E402
 
 base, Q = make_latent16(n=1_000_000, d=128, m=10_000, seed=1234)
 h, _ = ga.build(ga.Dataset(base), ga.BuildConfig(seed=7))
-for pq, vs, tau in ((256, 512, 0.58), (1024, 2048, 0.58), (1024, 2048, 2.0)):
-    cfg = ga.QueryConfig(k_out=10, tau=tau, prioq_size=pq, visited_size=vs, max_iterations=2048)
+for pq, vs, tau in ((256, 512, 0.58), (1024, 2048, 0.58), (1024, 2048, 2.0), (2048, 4096, 1.0)):
+    cfg = ga.QueryConfig(k_out=10, tau=tau, prioq_size=pq, visited_size=vs, max_iterations=4 * pq)
     for _ in range(3):
         ga.query_arrays(h, Q, cfg, out="device")
     torch.cuda.synchronize()
