@@ -527,7 +527,10 @@ struct WarpSearch {
         // key exceeds thr >= every admitted key, so counting smaller keys
         // over all nc candidates already ranks the admitted ones among
         // themselves.  Keys < 2^31: (kj - key) >> 31 == (kj < key).
-        const bool adm = lane < nc && KO::to_d(key) <= thr;
+        // integer keys: key <= thr  <=>  key <= floor(thr) (thr >= 0), one
+        // conversion per step instead of one FP64 compare per lane
+        const uint32_t thr_u = thr < 4294967295.0 ? (uint32_t)thr : 0xffffffffu;
+        const bool adm = lane < nc && (uint32_t)key <= thr_u;
         const unsigned am = __ballot_sync(FULL, adm);
         m = __popc(am);
         forgotten += nc - m;
