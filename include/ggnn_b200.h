@@ -133,7 +133,8 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
  * host-to-host path overlaps the upload with the search): rows
  * [c * chunk_rows, (c + 1) * chunk_rows) of d_q_f32 may be read once
  * d_chunk_flags[c] == epoch, which the caller's copy stream writes after the
- * rows.  narrow != 0 (uint8 tables): rows are narrowed to uint8 on load and a
+ * rows; d_chunk_flags == NULL means every row is already readable (e.g. the
+ * device address of pinned host memory).  narrow != 0 (uint8 tables): rows are narrowed to uint8 on load and a
  * value that is not an integer in [0, 255] sets bit 0 of *d_status; a chunk
  * that does not arrive within ~50 ms sets bit 1.  Either bit voids the
  * results (the caller reruns).  distinct_touched is not tracked. */
@@ -149,7 +150,10 @@ int ggnn_query_batch_staged(const ggnn_vectors *X, const ggnn_layer *bottom, con
  * *h_epoch), all queued before ggnn_query_batch_staged is launched on
  * search_stream (which then overlaps the chunks still in flight); the
  * results (and status, see above) are copied back into the pinned h_*
- * buffers on search_stream.  Asynchronous: the caller synchronises both
+ * buffers on search_stream.  When h_q and h_ids / h_dists / h_counters are
+ * all page-locked, the search instead reads the rows and writes the results
+ * through their mapped device addresses (zero copy; GGNN_ZERO_COPY=0 turns it
+ * off) and d_q_stage / d_chunk_flags are unused.  Asynchronous: the caller synchronises both
  * streams, checks *h_status == 0, and must not change *h_epoch or reuse the
  * staging buffers before that. */
 int ggnn_query_batch_host(const ggnn_vectors *X, const ggnn_layer *bottom, const int32_t *d_top_rows, int64_t ntop,

@@ -202,6 +202,7 @@ __device__ __forceinline__ int64_t next_item(int* work, WorkCursor& w) {
 // acquire at system scope would invalidate the SM's L1 at every query start,
 // throwing away the other searches' prefetched rows.
 __device__ __forceinline__ void wait_query_chunk(const SearchArgs& a, int64_t qi) {
+  if (!a.qflags) return;  // zero-copy: the rows are read straight from mapped host memory
   if (lane_id() == 0) {
     const volatile uint32_t* f = a.qflags + qi / a.qchunk;
     uint32_t v = *f;
@@ -1184,7 +1185,7 @@ int ggnn_query_batch_staged(const ggnn_vectors* X, const ggnn_layer* bottom, con
                             const float* d_q_f32, int64_t m, const ggnn_search_params* p, double d_nn1_max,
                             const uint32_t* d_chunk_flags, int64_t chunk_rows, uint32_t epoch, int32_t narrow,
                             int32_t* d_ids, double* d_dists, int32_t* d_counters, int32_t* d_status, void* stream) {
-  GGNN_CHECK_ARG(X && d_q_f32 && d_chunk_flags && chunk_rows >= 1 && d_status, "invalid staged query arguments");
+  GGNN_CHECK_ARG(X && d_q_f32 && (!d_chunk_flags || chunk_rows >= 1) && d_status, "invalid staged query arguments");
   GGNN_CHECK_ARG(!narrow || X->dtype == GGNN_U8, "narrowing needs a uint8 table");
   ggnn_queries Q;
   Q.d_data = d_q_f32;
@@ -1225,6 +1226,24 @@ int ggnn_query_batch_staged(const ggnn_vectors* X, const ggnn_layer* bottom, con
   }
 }
 
+// Device address of a page-locked host buffer, or nullptr for pageable memory.
+static void* mapped_host(const void* h) {
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return pa.type == cudaMemoryTypeHost ? pa.devicePointer : nullptr;
+}
+
+static bool zero_copy_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GGNN_ZERO_COPY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int ggnn_query_batch_host(const ggnn_vectors* X, const ggnn_layer* bottom, const int32_t* d_top_rows, int64_t ntop,
                           const float* h_q, int64_t m, const ggnn_search_params* p, double d_nn1_max, float* d_q_stage,
                           uint32_t* d_chunk_flags, const uint32_t* h_epoch, int32_t nchunks, int32_t narrow,
@@ -1247,6 +1266,23 @@ int ggnn_query_batch_host(const ggnn_vectors* X, const ggnn_layer* bottom, const
     return GGNN_OK;
   };
   GGNN_CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t), ss));
+  // Zero copy: when the query rows and the three result arrays are pinned
+  // (page-locked host memory is mapped into the device's address space) the
+  // search reads each query row over PCIe as its warp starts it and writes
+  // its hits back as it finishes: no upload chunks, no flags and no trailing
+  // device-to-host copies -- the transfers hide under the search itself.
+  const void* zq = mapped_host(h_q);
+  void* zi = mapped_host(h_ids);
+  void* zd = mapped_host(h_dists);
+  void* zc = mapped_host(h_counters);
+  if (zq && zi && zd && zc && zero_copy_enabled()) {
+    int rc = ggnn_query_batch_staged(X, bottom, d_top_rows, ntop, static_cast<const float*>(zq), m, p, d_nn1_max,
+                                     nullptr, 1, 0, narrow, static_cast<int32_t*>(zi), static_cast<double*>(zd),
+                                     static_cast<int32_t*>(zc), d_status, search_stream);
+    if (rc) return rc;
+    GGNN_CUDA_TRY(cudaMemcpyAsync(h_status, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
+    return GGNN_OK;
+  }
   // Every upload is queued before the search is launched: from pinned memory
   // the queueing is asynchronous, so the search still starts while the
   // chunks are in flight, and when the two streams cannot overlap (a

@@ -253,6 +253,29 @@ def test_staged_host_path_equals_chunked(golden_sift):
     np.testing.assert_array_equal(c.dists, d.dists)
 
 
+def test_zero_copy_host_path_equals_chunked(golden_sift):
+    """Page-locked query rows take the zero-copy host path (the search reads
+    the rows and writes its hits through mapped host memory): identical to the
+    chunked upload of the same rows from pageable memory, fractional rows
+    included (reported, then answered by the float search)."""
+    import torch
+
+    g, h, queries = golden_sift
+    cfg = ga.QueryConfig(k_out=10, tau=0.6)
+    reps = -(-3001 // len(queries))
+    Q = np.ascontiguousarray(np.tile(queries, (reps, 1))[:3001]).astype(np.float32)
+    for frac in (False, True):
+        if frac:
+            Q[2000, 5] += 0.25
+        pinned = torch.from_numpy(Q).pin_memory()
+        a = ga.query_arrays(h, Q, cfg)
+        b = ga.query_arrays(h, pinned.numpy(), cfg)
+        np.testing.assert_array_equal(a.ids, b.ids)
+        np.testing.assert_array_equal(a.dists, b.dists)
+        np.testing.assert_array_equal(a.counters, b.counters)
+    np.testing.assert_array_equal(b.ids[: len(queries)], g["q6_ids"])
+
+
 def test_staged_host_path_float_table():
     """Float tables take the chunked host path (the staged one is for uint8
     tables): with and without the staged switch, equal to the

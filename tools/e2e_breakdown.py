@@ -18,7 +18,7 @@ from paper_1912_01059_b200.synthetic import make_latent16  # noqa: E402
 
 base, Q = make_latent16(n=1_000_000, d=128, m=10_000, seed=1234)
 h, _ = ga.build(ga.Dataset(base), ga.BuildConfig(seed=7))
-cfg = ga.QueryConfig(k_out=10, tau=0.6)
+cfg = ga.QueryConfig(k_out=10, tau=0.58)
 Qp = torch.empty(Q.shape, dtype=torch.float32, pin_memory=True)
 Qp.copy_(torch.from_numpy(np.ascontiguousarray(Q, dtype=np.float32)))
 Q = Qp.numpy()
