@@ -78,6 +78,7 @@ _SIGS = {
     "ggnn_leaf_knn_tc": [P, P, P, P, I64, I64, I32, P, P, P, I32, P, P, P, P],
     "ggnn_tc_timeouts": [],
     "ggnn_search_accounting": [P],
+    "ggnn_query_schedule": [I64, F64],
     "ggnn_merge_descent": [P, P, I32, I32, I32, P, I64, P, I32, I32, P, P, P, P, P],
     "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_merge_rows_range": [I64, I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],

@@ -159,7 +159,32 @@ struct SearchArgs {
   int qconv;
   int32_t* qstatus;
   unsigned long long* acc;  // build accounting (visited, steps) or nullptr
+  // longest-first schedule (launch_query): pilot > 0 runs every search for at
+  // most `pilot` expansions and parks the open ones (park_key: a predicted
+  // length bucket, PARK_DONE when finished); the resume pass takes them in
+  // park_order
+  long long pilot;
+  uint8_t* park;
+  size_t park_slot;
+  uint32_t* park_key;
+  const int32_t* park_order;
+  const int32_t* park_count;
 };
+
+constexpr uint32_t PARK_DONE = 0xffffffffu;
+constexpr int PARK_BUCKETS = 1024;
+
+// Predicted search length of a parked search: its best distance so far, in
+// eighth-octave buckets (larger = longer).  Measured on C2 pilots of 16-24
+// expansions, this ranks the remaining work with Spearman 0.5-0.6 -- enough
+// to start most of the longest searches in the first wave
+// (tools/drain_data.py).
+__device__ __forceinline__ uint32_t park_bucket(double d1) {
+  const float v = (float)d1;
+  if (!(v > 0.0f)) return 0u;
+  const float b = (log2f(v) + 64.0f) * 8.0f;
+  return b <= 0.0f ? 0u : (b >= (float)(PARK_BUCKETS - 1) ? (uint32_t)(PARK_BUCKETS - 1) : (uint32_t)b);
+}
 
 // Persistent warps: with a work counter (zeroed before the launch) every warp
 // takes the next items when it finishes one, so uneven search lengths never
@@ -292,12 +317,19 @@ __device__ void write_hits(WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64
                            int extra_visited, int extra_distinct) {
   const int k_out = a.c.k_out;
   s.write_out(to_row, (a.c.flags & FLAG_EXACT_DISTS) != 0, a.ids + qi * k_out, a.dists + qi * k_out);
+#ifdef GGNN_DEBUG_OPEN
+  extra_distinct = s.open_work();
+#endif
   if (lane_id() == 0 && a.counters) {
     int32_t* c = a.counters + qi * 5;
     c[0] = s.visited + extra_visited;
     c[1] = s.steps;
     c[2] = s.term;
+#ifdef GGNN_DEBUG_OPEN
+    c[3] = extra_distinct;
+#else
     c[3] = a.ever == nullptr ? -1 : extra_distinct;  // + the log's distinct ids (distinct_log_kernel)
+#endif
     c[4] = s.forgotten;
   }
   finish_log(s, a, qi);
@@ -356,7 +388,16 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
     if (lane < kc) sid = a.top_rows ? __ldg(a.top_rows + bi) : bi;
     s.seed(bk, sid, kc);
   }
-  s.run();
+  if (!PUSH && a.pilot > 0) {
+    if (s.run_until(a.pilot)) {
+      s.park(a.park + (size_t)qi * a.park_slot, a.d * (int64_t)sizeof(TQ));
+      if (lane == 0) a.park_key[qi] = park_bucket(KeyOps<Key>::to_d(s.ring_key(0)));
+      return;
+    }
+    if (lane == 0) a.park_key[qi] = PARK_DONE;
+  } else {
+    s.run();
+  }
   // query() adds the top scan to the effort counters (search.py:134-136)
   write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
   if constexpr (PUSH) {
@@ -380,6 +421,75 @@ __global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeo
   } else {
     const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (qi < a.m) query_kernel_one<TX, TQ, LP, PUSH, STAGED>(a, smem_w, vring_lane, qi);
+  }
+}
+
+// Resume pass of the longest-first schedule: warp w continues parked search
+// park_order[w] to its end.
+template <typename TX, typename TQ, int LP>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) resume_kernel(const __grid_constant__ SearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (int64_t)*a.park_count) return;
+  const int64_t qi = a.park_order[w];
+  uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
+  WarpSearch<TX, TQ, LP> s;
+  s.vr = vring_lane;
+  init_search(s, a, smem_w, qi);
+  set_layer(s, a.layer);
+  s.dmax = a.dmax;
+  s.reset();
+  s.unpark(a.park + (size_t)qi * a.park_slot, a.d * (int64_t)sizeof(TQ));
+  s.run();
+  const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
+  write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
+}
+
+// Parked searches in descending bucket order (one CTA; the order inside a
+// bucket is arbitrary -- it only schedules, results do not depend on it).
+__global__ void __launch_bounds__(PARK_BUCKETS) park_order_kernel(const uint32_t* key, int64_t m, int32_t* order,
+                                                                  int32_t* count) {
+  __shared__ int hist[PARK_BUCKETS];
+  __shared__ int wsum[PARK_BUCKETS / 32];
+  const int t = threadIdx.x;
+  hist[t] = 0;
+  __syncthreads();
+  for (int64_t i = t; i < m; i += PARK_BUCKETS) {
+    const uint32_t k = key[i];
+    if (k != PARK_DONE) atomicAdd(&hist[k], 1);
+  }
+  __syncthreads();
+  // exclusive scan over buckets from the highest down: thread t owns bucket
+  // PARK_BUCKETS - 1 - t
+  const int b = PARK_BUCKETS - 1 - t;
+  const int v = hist[b];
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, x, o);
+    if ((t & 31) >= o) x += y;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = x;
+  __syncthreads();
+  if (t < 32) {
+    int z = wsum[t];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, z, o);
+      if (t >= o) z += y;
+    }
+    wsum[t] = z;  // inclusive over warps
+  }
+  __syncthreads();
+  const int excl = x - v + ((t >> 5) ? wsum[(t >> 5) - 1] : 0);
+  __syncthreads();
+  hist[b] = excl;
+  if (t == PARK_BUCKETS - 1) *count = excl + v;
+  __syncthreads();
+  for (int64_t i = t; i < m; i += PARK_BUCKETS) {
+    const uint32_t k = key[i];
+    if (k != PARK_DONE) order[atomicAdd(&hist[k], 1)] = (int32_t)i;
   }
 }
 
@@ -909,6 +1019,111 @@ int launch_static(Kern kern, const SearchArgs& a, int64_t items, size_t region, 
   return launch_items(kern, a, items, region, st, want, false);
 }
 
+// ---- longest-first schedule of a query batch --------------------------------
+// A batch of m searches on R resident warps runs in m / R waves; the launch
+// ends when its longest searches do, and under FIFO some of those start in the
+// last wave (C2: 1.88 ms per 10k queries against 1.22 ms when the same batch is
+// launched longest-first).  So every search first runs a pilot of P
+// expansions (GGNN_PILOT, default 20; 0 disables), the open ones are parked
+// with a predicted-length bucket, sorted by one CTA, and resumed
+// longest-predicted first.  Used for batches of at least 1.5 waves that need
+// no distinct_touched logs; results are step-by-step those of the plain launch.
+constexpr size_t PARK_MAX_BYTES = size_t(4) << 30;
+
+long long g_pilot = -1;        // < 0: GGNN_PILOT or the default
+double g_min_waves = 1.5;       // batches of fewer waves launch plainly
+
+long long pilot_steps() {
+  if (g_pilot >= 0) return g_pilot;
+  static const long long P = [] {
+    const char* e = getenv("GGNN_PILOT");
+    return e ? atoll(e) : 20LL;
+  }();
+  return P;
+}
+
+// stream-ordered park buffers stay in the device's default pool between
+// batches instead of being returned to the driver at every synchronisation
+void keep_default_pool() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+template <typename Kern>
+int64_t resident_searches(Kern kern, size_t region) {
+  const int W = pick_warps(region, SEARCH_WARPS);
+  if (W <= 0) return 0;
+  const size_t smem = (size_t)W * region + GGNN_SMEM_PAD;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem) != cudaSuccess) return 0;
+  return (int64_t)per_sm * W * std::max(dev_info().sm_count, 1);
+}
+
+template <typename TX, typename TQ, int LP, bool STAGED>
+int launch_query(SearchArgs a, cudaStream_t st) {
+  auto qk = query_kernel<TX, TQ, LP, false, STAGED>;
+  const long long P = pilot_steps();
+  const size_t slot = WarpSearch<TX, TQ, LP>::park_bytes(a.c, a.d * (int64_t)sizeof(TQ));
+  const size_t bytes = (size_t)a.m * (slot + 8) + 16;
+  bool sched = P > 0 && !a.ever && a.m > 0 && bytes <= PARK_MAX_BYTES && a.c.max_steps > P;
+  if (sched) {
+    const int64_t res = resident_searches(qk, a.region);
+    sched = res > 0 && (double)a.m >= g_min_waves * (double)res;
+  }
+  if (!sched) return launch_warps(qk, a, a.m, a.region, st);
+  keep_default_pool();
+  uint8_t* buf = nullptr;
+  GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, st));
+  a.pilot = P;
+  a.park = buf;
+  a.park_slot = slot;
+  a.park_key = reinterpret_cast<uint32_t*>(buf + (size_t)a.m * slot);
+  int32_t* order = reinterpret_cast<int32_t*>(buf + (size_t)a.m * (slot + 4));
+  int32_t* count = reinterpret_cast<int32_t*>(buf + (size_t)a.m * (slot + 8));
+  int rc = launch_warps(qk, a, a.m, a.region, st);
+  if (rc == GGNN_OK) {
+    park_order_kernel<<<1, PARK_BUCKETS, 0, st>>>(a.park_key, a.m, order, count);
+    rc = cudaGetLastError() == cudaSuccess ? GGNN_OK : GGNN_E_CUDA;
+    if (rc) set_error("park_order_kernel launch failed");
+  }
+  if (rc == GGNN_OK) {
+    SearchArgs b = a;
+    b.pilot = 0;
+    b.park_order = order;
+    b.park_count = count;
+    rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS);
+  }
+  cudaFreeAsync(buf, st);
+  return rc;
+}
+
+template <bool STAGED>
+int launch_query_combo(const SearchArgs& a, int cmb, cudaStream_t st) {
+  switch (cmb) {
+    case 0:
+      if (a.lpr == 8) return launch_query<float, float, 8, STAGED>(a, st);
+      if (a.lpr == 32) return launch_query<float, float, 32, STAGED>(a, st);
+      return launch_query<float, float, 0, STAGED>(a, st);
+    case 1:
+      if (a.lpr == 8) return launch_query<uint8_t, uint8_t, 8, STAGED>(a, st);
+      if (a.lpr == 32) return launch_query<uint8_t, uint8_t, 32, STAGED>(a, st);
+      return launch_query<uint8_t, uint8_t, 0, STAGED>(a, st);
+    default:
+      return launch_query<uint8_t, float, 0, STAGED>(a, st);
+  }
+}
+
 // Launch the LP-specialised instantiation matching a.lpr (see warp_dists_t).
 #define GGNN_LAUNCH_LP(KER, TX, TQ, ...)                                          \
   (a.lpr == 8    ? launch_warps(KER<TX, TQ, 8>, __VA_ARGS__)                     \
@@ -1056,6 +1271,13 @@ int ggnn_search_accounting(unsigned long long* d_acc) {
   g_acc = d_acc;
   return GGNN_OK;
 }
+int ggnn_query_schedule(long long pilot_steps, double min_waves) {
+  GGNN_CHECK_ARG(min_waves >= 0.0, "min_waves must be >= 0");
+  g_pilot = pilot_steps;
+  g_min_waves = min_waves;
+  return GGNN_OK;
+}
+
 int ggnn_version(void) { return 100; }
 
 int ggnn_device_info(int* sm_count, int* smem_per_block) {
@@ -1125,11 +1347,7 @@ int ggnn_query_batch(const ggnn_vectors* X, const ggnn_layer* bottom, const int3
   rc = attach_ever(a, p, p->k_out, bottom->k, d_workspace, workspace_bytes);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  switch (combo(X, Q)) {
-    case 0: rc = GGNN_LAUNCH_LP(query_kernel, float, float, a, a.m, a.region, st); break;
-    case 1: rc = GGNN_LAUNCH_LP(query_kernel, uint8_t, uint8_t, a, a.m, a.region, st); break;
-    default: rc = launch_warps(query_kernel<uint8_t, float, 0>, a, a.m, a.region, st); break;
-  }
+  rc = launch_query_combo<false>(a, combo(X, Q), st);
   return rc ? rc : count_distinct(a, st);
 }
 
@@ -1213,17 +1431,7 @@ int ggnn_query_batch_staged(const ggnn_vectors* X, const ggnn_layer* bottom, con
   a.qconv = narrow ? 1 : 0;
   a.qstatus = d_status;
   cudaStream_t st = as_stream(stream);
-  switch (combo(X, &Q)) {
-    case 0:
-      if (a.lpr == 32) return launch_warps(query_kernel<float, float, 32, false, true>, a, a.m, a.region, st);
-      if (a.lpr == 8) return launch_warps(query_kernel<float, float, 8, false, true>, a, a.m, a.region, st);
-      return launch_warps(query_kernel<float, float, 0, false, true>, a, a.m, a.region, st);
-    case 1:
-      if (a.lpr == 32) return launch_warps(query_kernel<uint8_t, uint8_t, 32, false, true>, a, a.m, a.region, st);
-      if (a.lpr == 8) return launch_warps(query_kernel<uint8_t, uint8_t, 8, false, true>, a, a.m, a.region, st);
-      return launch_warps(query_kernel<uint8_t, uint8_t, 0, false, true>, a, a.m, a.region, st);
-    default: return launch_warps(query_kernel<uint8_t, float, 0, false, true>, a, a.m, a.region, st);
-  }
+  return launch_query_combo<true>(a, combo(X, &Q), st);
 }
 
 // Device address of a page-locked host buffer, or nullptr for pageable memory.

@@ -613,6 +613,94 @@ struct WarpSearch {
     }
   }
 
+#ifdef GGNN_DEBUG_OPEN
+  // scheduling study only: unexpanded ring entries within the stopping
+  // threshold (the search's pending work when it was cut off)
+  __device__ int open_work() {
+    double thr = __longlong_as_double(0x7ff0000000000000ll);
+    if (L >= c.k_out)
+      thr = __dadd_rn(KO::to_d(ring_key(c.k_out - 1)), __dmul_rn(c.tau, fmin(dmax, KO::to_d(ring_key(0)))));
+    int n = 0;
+    for (int i = lane_id(); i < L; i += 32) n += (!rvis[i] && KO::to_d(ring_key(i)) <= thr) ? 1 : 0;
+    return warp_sum(n);
+  }
+#endif
+
+  // Run at most `limit` expansions in total; true while the search is still
+  // open (the pilot pass of the longest-first schedule, see park()).
+  __device__ __forceinline__ bool run_until(long long limit) {
+    while ((long long)steps < limit)
+      if (!step()) return false;
+    return true;
+  }
+
+  // Park / unpark an open search (the longest-first schedule of the query
+  // batch: every search first runs a short pilot, the open ones are parked
+  // and resumed longest-predicted first).  Parked: the ring and its visited
+  // flags (and a shared visited ring) -- the region's bytes below the
+  // refcount table --, the query row, the lane-held visited ring and the
+  // scalars.  The refcount table is rebuilt from the ring and the visited
+  // ring on unpark: its counts are exact functions of the two, tombstones
+  // only affect probing speed.  Step-by-step identical to an uninterrupted
+  // search.
+  static __host__ __device__ size_t park_bytes(const SearchCfg& c, int64_t qbytes) {
+    return 64 + (size_t)c.o_ht + align16((size_t)qbytes) + (vring_local(c.vsz) ? align16((size_t)c.vsz * 4) : 0);
+  }
+  __device__ __forceinline__ uint8_t* region_base() const {
+    if constexpr (PACK) return reinterpret_cast<uint8_t*>(re);
+    else return reinterpret_cast<uint8_t*>(rk);
+  }
+  __device__ void park(uint8_t* dst, int64_t qbytes) {
+    const int lane = lane_id();
+    __syncwarp();
+    if (lane == 0) {
+      int* h = reinterpret_cast<int*>(dst);
+      h[0] = L;
+      h[1] = vlen;
+      h[2] = vpos;
+      h[3] = visited;
+      h[4] = steps;
+      h[5] = distinct;
+      h[6] = forgotten;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(region_base());
+    uint4* o = reinterpret_cast<uint4*>(dst + 64);
+    for (int i = lane; i < (int)(c.o_ht / 16); i += 32) o[i] = src[i];
+    uint8_t* oq = dst + 64 + c.o_ht;
+    const uint8_t* q = reinterpret_cast<const uint8_t*>(qs);
+    for (int64_t i = lane * 4; i < qbytes; i += 128)
+      *reinterpret_cast<uint32_t*>(oq + i) = *reinterpret_cast<const uint32_t*>(q + i);
+    if (!vring) {
+      int* ov = reinterpret_cast<int*>(oq + align16((size_t)qbytes));
+      for (int j = 0; j < ((vlen + 31) >> 5); ++j) ov[j * 32 + lane] = vr[j];
+    }
+  }
+  // (after carve + set_layer + reset)
+  __device__ void unpark(const uint8_t* srcp, int64_t qbytes) {
+    const int lane = lane_id();
+    const int* h = reinterpret_cast<const int*>(srcp);
+    L = h[0];
+    vlen = h[1];
+    vpos = h[2];
+    visited = h[3];
+    steps = h[4];
+    distinct = h[5];
+    forgotten = h[6];
+    const uint4* src = reinterpret_cast<const uint4*>(srcp + 64);
+    uint4* o = reinterpret_cast<uint4*>(region_base());
+    for (int i = lane; i < (int)(c.o_ht / 16); i += 32) o[i] = src[i];
+    const uint8_t* sq = srcp + 64 + c.o_ht;
+    uint8_t* q = reinterpret_cast<uint8_t*>(qs);
+    for (int64_t i = lane * 4; i < qbytes; i += 128)
+      *reinterpret_cast<uint32_t*>(q + i) = *reinterpret_cast<const uint32_t*>(sq + i);
+    if (!vring) {
+      const int* sv = reinterpret_cast<const int*>(sq + align16((size_t)qbytes));
+      for (int j = 0; j < ((vlen + 31) >> 5); ++j) vr[j] = sv[j * 32 + lane];
+    }
+    __syncwarp();
+    rebuild();
+  }
+
   __device__ void run() {
     while (step()) {
     }

@@ -451,3 +451,64 @@ def test_k_out_above_32_descent_vs_checker(golden_sift):
         np.testing.assert_array_equal(r.dists, dists)
         assert (r.visited_count, r.steps, TERM_CODE[r.terminated_by], r.distinct_touched, r.forgotten) == (
             v, t, term, dist_cnt, fg)
+
+
+@pytest.fixture
+def schedule():
+    """Force the longest-first schedule (pilot, park, resume) on any batch
+    size: schedule(P) with P = 0 the plain launch."""
+    yield lambda p: N.call("ggnn_query_schedule", p, 0.0)
+    N.call("ggnn_query_schedule", -1, 1.5)
+
+
+def _arrays(h, Q, cfg, host=True):
+    if host:
+        r = ga.query_arrays(h, Q, cfg)
+        return r.ids, r.dists, r.counters
+    ids, dists, cnt = ga.query_arrays(h, Q, cfg, out="device")
+    return ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy()
+
+
+def test_longest_first_schedule_bitwise(golden_sift, schedule):
+    """Parking a search after a pilot of P expansions and resuming it later
+    (ring, visited flags, lane-held or shared visited ring, query row and
+    counters saved; the refcount table rebuilt) gives step-by-step the plain
+    search: identical ids, distances and counters for every P, on the host
+    (staged, uint8 narrowing) and device paths, for k_out <= 32 and > 32, a
+    visited ring too large for the lanes, and the golden answers."""
+    g, h, queries = golden_sift
+    reps = -(-2100 // len(queries))
+    Q = np.ascontiguousarray(np.tile(queries, (reps, 1))[:2100]).astype(np.float32)
+    cases = [ga.QueryConfig(k_out=10, tau=0.6), ga.QueryConfig(k_out=40, tau=0.6, prioq_size=96),
+             ga.QueryConfig(k_out=10, tau=0.8, prioq_size=300, visited_size=5000, max_iterations=3000)]
+    for cfg in cases:
+        for host in (True, False):
+            schedule(0)
+            want = _arrays(h, Q, cfg, host)
+            for P in (1, 7, 20):
+                schedule(P)
+                got = _arrays(h, Q, cfg, host)
+                for w, x in zip(want, got):
+                    np.testing.assert_array_equal(w, x)
+    schedule(20)
+    np.testing.assert_array_equal(_arrays(h, Q, cases[0])[0][: len(queries)], g["q6_ids"])
+
+
+def test_longest_first_schedule_float_and_mixed(schedule):
+    """The same on a float table (FP64 keys, exact re-score) and on a uint8
+    table searched with fractional float queries (mixed key path)."""
+    from paper_1912_01059_b200.synthetic import make_latent16
+
+    base, Q = make_latent16(n=6000, d=64, m=1800, seed=5)
+    hf, _ = ga.build(ga.Dataset((base / 255.0).astype(np.float32)), ga.BuildConfig(seed=7))
+    hu, _ = ga.build(ga.Dataset(base), ga.BuildConfig(seed=7))
+    Qf = (Q / 255.0).astype(np.float32)
+    Qm = Q.astype(np.float32) + np.float32(0.25)
+    cfg = ga.QueryConfig(k_out=10, tau=0.5)
+    for h, q in ((hf, Qf), (hu, Qm)):
+        schedule(0)
+        want = _arrays(h, q, cfg)
+        schedule(9)
+        got = _arrays(h, q, cfg)
+        for w, x in zip(want, got):
+            np.testing.assert_array_equal(w, x)
