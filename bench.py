@@ -631,19 +631,24 @@ def run_index(args, dist, torch):
         pinned.append(t_.numpy())
     # (at least 20 untimed calls: the first few dozen host-side calls of a
     # process run measurably slower -- allocator and interpreter warm-up)
-    for i in range(max(20, args.warmup)):
-        ga.query_arrays(h, pinned[i % B], qcfg)
+    for i in range(max(20, args.warmup)):  # as the timed loop: the previous result stays alive
+        out = ga.query_arrays(h, pinned[i % B], qcfg)
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
+    call_t = []
     for i in range(args.steps):
+        c0 = time.perf_counter()
         out = ga.query_arrays(h, pinned[i % B], qcfg)
+        call_t.append(time.perf_counter() - c0)
     torch.cuda.synchronize()
     e2e_t = dist.max(time.perf_counter() - t0)
     out0 = ga.query_arrays(h, pinned[0], qcfg)
     e2e = {"value": G * m * args.steps / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(pinned[0].nbytes),
            "d2h_bytes_per_step": int(out.ids.nbytes + out.dists.nbytes + out.counters.nbytes + 4),
-           "api": "paper_1912_01059_b200.query_arrays(h, numpy float32 queries in pinned memory) -> host arrays"}
+           "api": "paper_1912_01059_b200.query_arrays(h, numpy float32 queries in pinned memory) -> host arrays",
+           "call_ms": {"min": round(min(call_t) * 1e3, 3), "median": round(float(np.median(call_t)) * 1e3, 3),
+                       "max": round(max(call_t) * 1e3, 3)}}
 
     # ---- CPU baselines (rank 0, N == 1) -------------------------------
     cpu, ref_build_res = None, None
@@ -858,7 +863,7 @@ def run_sharded(args, dist, torch):
         pinned.append(t_.numpy())
     exch = args.exchange if G > 1 else "nccl"
     for i in range(max(1, args.warmup)):
-        grp.query_arrays(pinned[i % B], qcfg, exchange=exch)
+        out = grp.query_arrays(pinned[i % B], qcfg, exchange=exch)
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()

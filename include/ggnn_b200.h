@@ -132,8 +132,10 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
  * host variants; no reference counterpart -- results never depend on it):
  * a batch of at least min_waves waves of resident searches first runs every
  * search for pilot_steps expansions, parks the open ones and resumes them
- * longest-predicted first.  pilot_steps < 0 restores the default (GGNN_PILOT,
- * else 20), 0 disables; min_waves defaults to 1.5.  Process-wide. */
+ * longest-predicted first (a second round up to GGNN_PILOT2 = 32 expansions
+ * re-parks them with a sharper prediction).  pilot_steps < 0 restores the
+ * default (GGNN_PILOT, else 8), 0 disables; min_waves defaults to 1.5.
+ * Process-wide. */
 int ggnn_query_schedule(long long pilot_steps, double min_waves);
 
 /* Replaces: query (search.py:115-137) for a batch, like ggnn_query_batch,

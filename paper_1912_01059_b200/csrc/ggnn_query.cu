@@ -164,6 +164,7 @@ struct SearchArgs {
   // length bucket, PARK_DONE when finished); the resume pass takes them in
   // park_order
   long long pilot;
+  float park_a;  // weight of log2(pending work + 1) in the length prediction
   uint8_t* park;
   size_t park_slot;
   uint32_t* park_key;
@@ -174,16 +175,27 @@ struct SearchArgs {
 constexpr uint32_t PARK_DONE = 0xffffffffu;
 constexpr int PARK_BUCKETS = 1024;
 
-// Predicted search length of a parked search: its best distance so far, in
-// eighth-octave buckets (larger = longer).  Measured on C2 pilots of 16-24
-// expansions, this ranks the remaining work with Spearman 0.5-0.6 -- enough
-// to start most of the longest searches in the first wave
+// Predicted search length of a parked search, in eighth-octave buckets
+// (larger = longer): log2 of its best distance so far plus park_a x log2 of
+// its pending work (unexpanded ring entries within the stopping threshold).
+// On C2 the best distance after 16-24 expansions ranks the remaining work
+// with Spearman 0.5-0.6, the pending work after 32 with 0.87 (but coarsely);
+// together they start most of the longest searches in the first wave
 // (tools/drain_data.py).
-__device__ __forceinline__ uint32_t park_bucket(double d1) {
+__device__ __forceinline__ uint32_t park_bucket(double d1, int open, float wa) {
   const float v = (float)d1;
-  if (!(v > 0.0f)) return 0u;
-  const float b = (log2f(v) + 64.0f) * 8.0f;
+  float b = 0.0f;
+  if (v > 0.0f) b = (log2f(v) + 64.0f) * 8.0f;
+  b += wa * 8.0f * log2f((float)open + 1.0f);
   return b <= 0.0f ? 0u : (b >= (float)(PARK_BUCKETS - 1) ? (uint32_t)(PARK_BUCKETS - 1) : (uint32_t)b);
+}
+
+template <typename TX, typename TQ, int LP>
+__device__ __forceinline__ void park_search(WarpSearch<TX, TQ, LP>& s, const SearchArgs& a, int64_t qi) {
+  using Key = typename VecTraits<TX, TQ>::Key;
+  const int open = a.park_a != 0.0f ? s.open_work() : 0;
+  s.park(a.park + (size_t)qi * a.park_slot, a.d * (int64_t)sizeof(TQ));
+  if (lane_id() == 0) a.park_key[qi] = park_bucket(KeyOps<Key>::to_d(s.ring_key(0)), open, a.park_a);
 }
 
 // Persistent warps: with a work counter (zeroed before the launch) every warp
@@ -388,16 +400,14 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
     if (lane < kc) sid = a.top_rows ? __ldg(a.top_rows + bi) : bi;
     s.seed(bk, sid, kc);
   }
-  if (!PUSH && a.pilot > 0) {
-    if (s.run_until(a.pilot)) {
-      s.park(a.park + (size_t)qi * a.park_slot, a.d * (int64_t)sizeof(TQ));
-      if (lane == 0) a.park_key[qi] = park_bucket(KeyOps<Key>::to_d(s.ring_key(0)));
-      return;
-    }
-    if (lane == 0) a.park_key[qi] = PARK_DONE;
-  } else {
-    s.run();
+  // one copy of the step loop (two inlined copies measured 2x slower: the
+  // instruction cache holds one); target = -1, so run() == run_until(inf)
+  const bool pilot = !PUSH && a.pilot > 0;
+  if (s.run_until(pilot ? a.pilot : LLONG_MAX)) {
+    park_search(s, a, qi);
+    return;
   }
+  if (pilot && lane == 0) a.park_key[qi] = PARK_DONE;
   // query() adds the top scan to the effort counters (search.py:134-136)
   write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
   if constexpr (PUSH) {
@@ -425,7 +435,8 @@ __global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeo
 }
 
 // Resume pass of the longest-first schedule: warp w continues parked search
-// park_order[w] to its end.
+// park_order[w] to its end, or (pilot > 0: an intermediate round) up to
+// `pilot` expansions in total and parks it again with a fresh prediction.
 template <typename TX, typename TQ, int LP>
 __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) resume_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -441,7 +452,11 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) resume_kern
   s.dmax = a.dmax;
   s.reset();
   s.unpark(a.park + (size_t)qi * a.park_slot, a.d * (int64_t)sizeof(TQ));
-  s.run();
+  if (s.run_until(a.pilot > 0 ? a.pilot : LLONG_MAX)) {  // one copy of the step loop
+    park_search(s, a, qi);
+    return;
+  }
+  if (a.pilot > 0 && lane_id() == 0) a.park_key[qi] = PARK_DONE;
   const int kk = (int)min((int64_t)a.c.k_out, a.ntop);
   write_hits(s, a, qi, a.layer.to_row, (int)a.ntop, (int)a.ntop - kk);
 }
@@ -1024,9 +1039,11 @@ int launch_static(Kern kern, const SearchArgs& a, int64_t items, size_t region, 
 // ends when its longest searches do, and under FIFO some of those start in the
 // last wave (C2: 1.88 ms per 10k queries against 1.22 ms when the same batch is
 // launched longest-first).  So every search first runs a pilot of P
-// expansions (GGNN_PILOT, default 20; 0 disables), the open ones are parked
-// with a predicted-length bucket, sorted by one CTA, and resumed
-// longest-predicted first.  Used for batches of at least 1.5 waves that need
+// expansions (GGNN_PILOT, default 8; 0 disables), the open ones are parked
+// with a predicted-length bucket and sorted by one CTA; a second round runs
+// them longest-predicted first up to GGNN_PILOT2 (default 32) expansions and
+// parks the still-open ones again with a sharper prediction; the last round
+// runs them to their ends, longest-predicted first (C2: 1.83 -> 1.53 ms).  Used for batches of at least 1.5 waves that need
 // no distinct_touched logs; results are step-by-step those of the plain launch.
 constexpr size_t PARK_MAX_BYTES = size_t(4) << 30;
 
@@ -1037,9 +1054,26 @@ long long pilot_steps() {
   if (g_pilot >= 0) return g_pilot;
   static const long long P = [] {
     const char* e = getenv("GGNN_PILOT");
-    return e ? atoll(e) : 20LL;
+    return e ? atoll(e) : 8LL;
   }();
   return P;
+}
+// second round: searches still open after the pilot run up to this many
+// expansions in total and are parked again with a better prediction (the
+// pending work is a sharper predictor later in the search); 0 = one round
+long long pilot2_steps() {
+  static const long long P = [] {
+    const char* e = getenv("GGNN_PILOT2");
+    return e ? atoll(e) : 32LL;
+  }();
+  return P;
+}
+float pilot_weight() {
+  static const float A = [] {
+    const char* e = getenv("GGNN_PILOT_A");
+    return e ? (float)atof(e) : 0.5f;
+  }();
+  return A;
 }
 
 // stream-ordered park buffers stay in the device's default pool between
@@ -1086,6 +1120,7 @@ int launch_query(SearchArgs a, cudaStream_t st) {
   uint8_t* buf = nullptr;
   GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, st));
   a.pilot = P;
+  a.park_a = pilot_weight();
   a.park = buf;
   a.park_slot = slot;
   a.park_key = reinterpret_cast<uint32_t*>(buf + (size_t)a.m * slot);
@@ -1097,11 +1132,21 @@ int launch_query(SearchArgs a, cudaStream_t st) {
     rc = cudaGetLastError() == cudaSuccess ? GGNN_OK : GGNN_E_CUDA;
     if (rc) set_error("park_order_kernel launch failed");
   }
+  const long long P2 = pilot2_steps();
+  SearchArgs b = a;
+  b.park_order = order;
+  b.park_count = count;
+  if (rc == GGNN_OK && P2 > P && a.c.max_steps > P2) {
+    b.pilot = P2;
+    rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS);
+    if (rc == GGNN_OK) {
+      park_order_kernel<<<1, PARK_BUCKETS, 0, st>>>(a.park_key, a.m, order, count);
+      rc = cudaGetLastError() == cudaSuccess ? GGNN_OK : GGNN_E_CUDA;
+      if (rc) set_error("park_order_kernel launch failed");
+    }
+  }
   if (rc == GGNN_OK) {
-    SearchArgs b = a;
     b.pilot = 0;
-    b.park_order = order;
-    b.park_count = count;
     rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS);
   }
   cudaFreeAsync(buf, st);

@@ -613,9 +613,8 @@ struct WarpSearch {
     }
   }
 
-#ifdef GGNN_DEBUG_OPEN
-  // scheduling study only: unexpanded ring entries within the stopping
-  // threshold (the search's pending work when it was cut off)
+  // unexpanded ring entries within the stopping threshold: the pending work
+  // of a search cut off by a step limit (longest-first schedule)
   __device__ int open_work() {
     double thr = __longlong_as_double(0x7ff0000000000000ll);
     if (L >= c.k_out)
@@ -624,7 +623,6 @@ struct WarpSearch {
     for (int i = lane_id(); i < L; i += 32) n += (!rvis[i] && KO::to_d(ring_key(i)) <= thr) ? 1 : 0;
     return warp_sum(n);
   }
-#endif
 
   // Run at most `limit` expansions in total; true while the search is still
   // open (the pilot pass of the longest-first schedule, see park()).

@@ -230,10 +230,12 @@ def _query_host_fast(dh, Q: np.ndarray, cfg: QueryConfig, distinct: bool = False
 
 def _query_host_fast_locked(dh, Q: np.ndarray, cfg: QueryConfig, distinct: bool = False) -> BatchResult:
     t = N.torch()
-    # staged: uint8 tables only (float32 rows stay float and their upload is
-    # 4x larger; measured slower than the chunked path on gist1m), and no
+    # staged: uint8 tables, and float tables whose query rows are page-locked
+    # (read in place by the search, zero copy; uploading float rows in flagged
+    # chunks measured slower than the chunked path on gist1m); no
     # distinct_touched logs
-    if _STAGED and not distinct and Q.shape[0] >= 1024 and dh.vectors.exact_integers:
+    if _STAGED and not distinct and Q.shape[0] >= 1024 and (
+            dh.vectors.exact_integers or t.from_numpy(Q).is_pinned()):
         r = _query_host_staged(dh, Q, cfg)
         if r is not None:
             return r

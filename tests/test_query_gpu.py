@@ -277,8 +277,8 @@ def test_zero_copy_host_path_equals_chunked(golden_sift):
 
 
 def test_staged_host_path_float_table():
-    """Float tables take the chunked host path (the staged one is for uint8
-    tables): with and without the staged switch, equal to the
+    """Float tables take the chunked host path from pageable rows and the
+    staged zero-copy one from page-locked rows: all equal to the
     device-resident call."""
     from paper_1912_01059_b200 import search as S
     from paper_1912_01059_b200.synthetic import make_latent16
@@ -295,6 +295,11 @@ def test_staged_host_path_float_table():
     finally:
         S._STAGED = True
     ids, dists, cnt = ga.query_arrays(h, Qf, cfg, out="device")
+    import torch
+
+    c = ga.query_arrays(h, torch.from_numpy(Qf).pin_memory().numpy(), cfg)  # staged, zero copy
+    for x, y in ((a.ids, c.ids), (a.dists, c.dists), (a.counters, c.counters)):
+        np.testing.assert_array_equal(x, y)
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dists, b.dists)
     np.testing.assert_array_equal(a.counters, b.counters)
@@ -485,7 +490,7 @@ def test_longest_first_schedule_bitwise(golden_sift, schedule):
         for host in (True, False):
             schedule(0)
             want = _arrays(h, Q, cfg, host)
-            for P in (1, 7, 20):
+            for P in (1, 7, 20, 40):
                 schedule(P)
                 got = _arrays(h, Q, cfg, host)
                 for w, x in zip(want, got):
