@@ -296,6 +296,42 @@ __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const 
   }
 }
 
+// The LP = 8 uint8 case of dists_u8_vec (rows of 5-8 16-byte chunks: the C2 /
+// C5 shapes) with its per-step overhead removed: every lane owns at most one
+// chunk, so the query chunk is loaded once, row addresses are one 32-bit
+// offset per group into a uint4 view of the table (no 64-bit pointer selects,
+// no null checks), and lanes past the row's last chunk load nothing.
+#ifndef GGNN_DISTS_V2
+#define GGNN_DISTS_V2 1
+#endif
+template <int UNR>
+__device__ __forceinline__ void dists_u8_lp8(const uint8_t* X, int64_t d, const uint8_t* qs, const int* rows, int cnt,
+                                             uint32_t* kout) {
+  constexpr int LPR = 8, RPP = 32 / LPR;
+  const int lane = lane_id();
+  const int sub = lane & (LPR - 1);
+  const int grp = lane >> 3;
+  const uint32_t nch = (uint32_t)(d >> 4);
+  const bool mine = (uint32_t)sub < nch;
+  const uint4* X4 = reinterpret_cast<const uint4*>(X) + sub;
+  const uint4 qv = mine ? reinterpret_cast<const uint4*>(qs)[sub] : make_uint4(0u, 0u, 0u, 0u);
+  for (int base = 0; base < cnt; base += RPP * UNR) {
+    uint4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int ci = base + u * RPP + grp;
+      v[u] = make_uint4(0u, 0u, 0u, 0u);
+      if (mine && ci < cnt) v[u] = __ldg(X4 + (size_t)(uint32_t)rows[ci] * nch);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint32_t t = group_reduce<LPR, uint32_t>(part_u8(v[u], qv));
+      const int ci = base + u * RPP + grp;
+      if (sub == 0 && ci < cnt) kout[ci] = t;
+    }
+  }
+}
+
 // scalar fallbacks (any d, any alignment): one row at a time, lanes stride d
 template <typename TX, typename TQ, typename Key>
 __device__ __forceinline__ void dists_scalar(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
@@ -357,7 +393,8 @@ template <typename TX, typename TQ, int LP>
 __device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
                                              typename VecTraits<TX, TQ>::Key* kout, int lpr) {
   if constexpr (LP == 8 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
-    dists_u8_vec<8, GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
+    if constexpr (GGNN_DISTS_V2 != 0) dists_u8_lp8<GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
+    else dists_u8_vec<8, GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
   } else if constexpr (LP == 32 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
     dists_u8_vec<32, 4>(X, d, qs, rows, cnt, kout);
   } else if constexpr (LP == 8 && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {

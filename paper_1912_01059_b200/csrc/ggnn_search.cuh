@@ -161,6 +161,12 @@ struct WarpSearch {
   int next_head;
   int visited, steps, distinct, forgotten, term;
   bool found_target;
+  // the stopping threshold, recomputed only after a merge placed a candidate
+  // among the first k_out ring entries (the only entries it depends on):
+  // integer keys keep floor(thr) (key <= thr <=> key <= floor(thr), thr >= 0)
+  bool thr_dirty;
+  uint32_t thr_u;
+  double thr_d;
 
   __device__ __forceinline__ Key ring_key(int i) const {
     if constexpr (PACK) return (Key)(re[i] >> 32);
@@ -199,6 +205,7 @@ struct WarpSearch {
     visited = steps = distinct = forgotten = 0;
     term = TERM_EMPTY;
     found_target = false;
+    thr_dirty = true;
   }
 
   // append lanes [0, n) with valid[lane] to the log (in lane order)
@@ -236,16 +243,18 @@ struct WarpSearch {
   __device__ int head_from(int start) const {
     const int lane = lane_id();
     for (int base = start & ~3; base < L; base += 128) {
-      int p0 = base + 4 * lane;
-      uint32_t w = *reinterpret_cast<const uint32_t*>(rvis + p0);
-      int fb = 4;
-#pragma unroll
-      for (int b = 3; b >= 0; --b)
-        if (p0 + b < L && p0 + b >= start && ((w >> (8 * b)) & 0xffu) == 0u) fb = b;
-      unsigned bal = __ballot_sync(FULL, fb < 4);
+      const int p0 = base + 4 * lane;
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(rvis + p0);
+      // visited flags are 0 / 1 bytes: bit 8b of z is set iff byte b is 0;
+      // keep the bytes at positions [start, L)
+      uint32_t z = ~w & 0x01010101u;
+      const int lo = start - p0, hi = L - p0;
+      if (lo > 0) z = lo >= 4 ? 0u : z & (0xffffffffu << (8 * lo));
+      if (hi < 4) z = hi <= 0 ? 0u : z & (0xffffffffu >> (32 - 8 * hi));
+      const unsigned bal = __ballot_sync(FULL, z != 0u);
       if (bal) {
-        int src = __ffs(bal) - 1;
-        return base + 4 * src + __shfl_sync(FULL, fb, src);
+        const int src = __ffs(bal) - 1;
+        return base + 4 * src + (__shfl_sync(FULL, __ffs(z), src) >> 3);
       }
     }
     return -1;
@@ -352,6 +361,7 @@ struct WarpSearch {
     // placed below o}.  Every source index is <= its destination and chunks
     // go downwards, so nothing is overwritten before it is read.
     const int p0 = __shfl_sync(FULL, p, 0);
+    if (p0 < c.k_out) thr_dirty = true;
     // chunks wholly above the last candidate's slot only move up by madm
     // (every candidate lies below them): a plain copy, no candidate masks
     const int pl = __shfl_sync(FULL, p, madm - 1);  // admitted lanes are the prefix [0, madm)
@@ -453,12 +463,20 @@ struct WarpSearch {
       term = TERM_EMPTY;
       return false;
     }
-    double thr = __longlong_as_double(0x7ff0000000000000ll);
-    // FP64, rounded exactly like the reference (no FMA contraction):
-    // thr = ring[k_out-1] + tau * min(d_nn1_max, ring[0])   (_core.pyx:241-244)
-    if (L >= c.k_out)
-      thr = __dadd_rn(KO::to_d(ring_key(c.k_out - 1)), __dmul_rn(c.tau, fmin(dmax, KO::to_d(ring_key(0)))));
-    if (KO::to_d(ring_key(pos)) > thr) {
+    if (thr_dirty) {
+      // FP64, rounded exactly like the reference (no FMA contraction):
+      // thr = ring[k_out-1] + tau * min(d_nn1_max, ring[0])   (_core.pyx:241-244)
+      double thr = __longlong_as_double(0x7ff0000000000000ll);
+      if (L >= c.k_out)
+        thr = __dadd_rn(KO::to_d(ring_key(c.k_out - 1)), __dmul_rn(c.tau, fmin(dmax, KO::to_d(ring_key(0)))));
+      if constexpr (PACK) thr_u = thr < 4294967295.0 ? (uint32_t)thr : 0xffffffffu;
+      else thr_d = thr;
+      thr_dirty = false;
+    }
+    bool stop;
+    if constexpr (PACK) stop = (uint32_t)ring_key(pos) > thr_u;
+    else stop = KO::to_d(ring_key(pos)) > thr_d;
+    if (stop) {
       term = TERM_STOP;
       return false;
     }
@@ -529,7 +547,6 @@ struct WarpSearch {
         // themselves.  Keys < 2^31: (kj - key) >> 31 == (kj < key).
         // integer keys: key <= thr  <=>  key <= floor(thr) (thr >= 0), one
         // conversion per step instead of one FP64 compare per lane
-        const uint32_t thr_u = thr < 4294967295.0 ? (uint32_t)thr : 0xffffffffu;
         const bool adm = lane < nc && (uint32_t)key <= thr_u;
         const unsigned am = __ballot_sync(FULL, adm);
         m = __popc(am);
@@ -572,7 +589,9 @@ struct WarpSearch {
       } else {
         // candidates are compacted into lanes [0, nc); crow / cid are free now
         warp_sort_n(key, id, nc, reinterpret_cast<uint64_t*>(crow));
-        const bool adm = lane < nc && KO::to_d(key) <= thr;
+        bool adm = lane < nc;
+        if constexpr (PACK) adm = adm && (uint32_t)key <= thr_u;
+        else adm = adm && KO::to_d(key) <= thr_d;
         m = __popc(__ballot_sync(FULL, adm));
         forgotten += nc - m;
         if (target >= 0) found = __any_sync(FULL, adm && id == target);

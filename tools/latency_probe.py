@@ -14,7 +14,12 @@ from paper_1912_01059_b200.device import device_hierarchy  # noqa: E402
 from paper_1912_01059_b200.synthetic import make_latent16  # noqa: E402
 
 base, Q = make_latent16(n=1_000_000, d=128, m=10_000, seed=1234)
+import time  # noqa: E402
+
+ga.build(ga.Dataset(base[:50_000]), ga.BuildConfig(seed=7))  # warm-up (module loading, allocator growth)
+t0 = time.perf_counter()
 h, _ = ga.build(ga.Dataset(base), ga.BuildConfig(seed=7))
+print(f"build {time.perf_counter() - t0:.2f} s", flush=True)
 dh = device_hierarchy(h)
 dv = dh.vectors
 tau = float(sys.argv[1]) if len(sys.argv) > 1 else 0.6
