@@ -33,6 +33,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 struct DevInfo {
   int sm_count;
   int smem_optin;
+  int smem_per_sm;  // shared memory per multiprocessor (bytes, incl. the 1 KB per CTA the runtime reserves)
 };
 DevInfo dev_info();
 

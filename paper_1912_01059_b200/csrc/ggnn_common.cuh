@@ -387,7 +387,7 @@ __device__ __forceinline__ void warp_dists(const TX* X, int64_t d, const TQ* qs,
 // LP == 0 keeps the runtime switch above.  LP must equal choose_lpr(...) of
 // the launch; mixed u8-data / float-query searches always use LP == 0.
 #ifndef GGNN_U8_UNR
-#define GGNN_U8_UNR 3  // row groups in flight for 128-byte uint8 rows: 12 rows ~ the mean candidate count (2 and 4 measured slower)
+#define GGNN_U8_UNR 4  // row groups in flight for 128-byte uint8 rows (dists_u8_lp8: 16 rows; 3 and 6 measured slower)
 #endif
 template <typename TX, typename TQ, int LP>
 __device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
@@ -539,8 +539,8 @@ struct RefTable {
       s = (s + 1) & mask;
     }
   }
-  __device__ __forceinline__ void clear() {
-    for (uint32_t i = lane_id(); i <= mask; i += 32) t[i] = EMPTY;
+  __device__ __forceinline__ void clear() {  // (tables of >= 64 slots, 16-byte aligned)
+    for (uint32_t i = 4u * lane_id(); i <= mask; i += 128u) *reinterpret_cast<uint4*>(t + i) = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
   }
 };

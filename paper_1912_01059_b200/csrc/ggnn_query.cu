@@ -50,13 +50,14 @@ void set_error(const char* fmt, ...) {
 }
 
 DevInfo dev_info() {
-  static DevInfo info{0, 0};
+  static DevInfo info{0, 0, 0};
   static std::once_flag once;
   std::call_once(once, [] {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&info.sm_count, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&info.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&info.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   });
   return info;
 }
@@ -78,6 +79,16 @@ constexpr int MAX_LAYERS = 24;
 constexpr int SEARCH_WARPS = GGNN_SEARCH_WARPS;
 constexpr int SEARCH_THREADS = 32 * SEARCH_WARPS;
 constexpr int SEARCH_MIN_BLOCKS = GGNN_SEARCH_MIN_BLOCKS;
+// uint8 table + uint8 queries: the packed ring (no flag bytes) leaves 6.6 KB
+// of shared memory per search, so more searches fit per SM when the register
+// budget allows it
+#ifndef GGNN_U8_MIN_BLOCKS
+#define GGNN_U8_MIN_BLOCKS GGNN_SEARCH_MIN_BLOCKS
+#endif
+template <typename TX, typename TQ>
+constexpr int min_blocks() {
+  return (sizeof(TX) == 1 && sizeof(TQ) == 1) ? GGNN_U8_MIN_BLOCKS / GGNN_SEARCH_WARPS : SEARCH_MIN_BLOCKS;
+}
 // the u8 query kernel fits 64 registers without spills (shared memory still
 // limits it to 28 warps/SM); the staged variant is capped there so its extra
 // load path does not change the search's code generation
@@ -419,7 +430,7 @@ __device__ __forceinline__ void query_kernel_one(const SearchArgs& a, uint8_t* s
 
 template <typename TX, typename TQ, int LP, bool PUSH = false, bool STAGED = false>
 __global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeof(TX) == 1) ? QUERY_MIN_BLOCKS
-                                                                                              : SEARCH_MIN_BLOCKS)
+                                                                                              : min_blocks<TX, TQ>())
     query_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
@@ -438,7 +449,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeo
 // park_order[w] to its end, or (pilot > 0: an intermediate round) up to
 // `pilot` expansions in total and parks it again with a fresh prediction.
 template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) resume_kernel(const __grid_constant__ SearchArgs a) {
+__global__ void __launch_bounds__(SEARCH_THREADS, min_blocks<TX, TQ>()) resume_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -536,7 +547,7 @@ __device__ __forceinline__ void greedy_kernel_one(const SearchArgs& a, uint8_t* 
 }
 
 template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) greedy_kernel(const __grid_constant__ SearchArgs a) {
+__global__ void __launch_bounds__(SEARCH_THREADS, min_blocks<TX, TQ>()) greedy_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
@@ -659,7 +670,7 @@ __device__ __forceinline__ void descent_kernel_one(const SearchArgs& a, uint8_t*
 }
 
 template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MIN_BLOCKS) descent_kernel(const __grid_constant__ SearchArgs a) {
+__global__ void __launch_bounds__(SEARCH_THREADS, min_blocks<TX, TQ>()) descent_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   uint8_t* smem_w = smem + (size_t)(threadIdx.x >> 5) * a.region;
@@ -1005,11 +1016,16 @@ int64_t persistent_grid(Kern kern, int threads, size_t smem, int64_t items_per_c
 }
 
 template <typename Kern, typename Args>
-int launch_items(Kern kern, Args a, int64_t items, size_t region, cudaStream_t st, int want, bool persistent = true) {
+int launch_items(Kern kern, Args a, int64_t items, size_t region, cudaStream_t st, int want, bool persistent = true,
+                 int occ_cap = 0) {
   if (items <= 0) return GGNN_OK;
   int W = pick_warps(region, want);
   GGNN_CHECK_ARG(W > 0, "search state of %zu bytes does not fit in shared memory", region);
   size_t smem = (size_t)W * region + GGNN_SMEM_PAD;
+  if (occ_cap > 0) {  // at most occ_cap CTAs per SM: pad the dynamic shared memory
+    const size_t per_cta = (size_t)dev_info().smem_per_sm / (size_t)occ_cap;
+    if (per_cta > smem + 1024) smem = std::min(per_cta - 1024, (size_t)dev_info().smem_optin);
+  }
   GGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t grid = (items + W - 1) / W;
   a.work = persistent ? work_counter(st) : nullptr;
@@ -1030,8 +1046,9 @@ int launch_warps(Kern kern, const SearchArgs& a, int64_t items, size_t region, c
 }
 // one item per warp (kernels without a work loop)
 template <typename Kern>
-int launch_static(Kern kern, const SearchArgs& a, int64_t items, size_t region, cudaStream_t st, int want) {
-  return launch_items(kern, a, items, region, st, want, false);
+int launch_static(Kern kern, const SearchArgs& a, int64_t items, size_t region, cudaStream_t st, int want,
+                  int occ_cap = 0) {
+  return launch_items(kern, a, items, region, st, want, false, occ_cap);
 }
 
 // ---- longest-first schedule of a query batch --------------------------------
@@ -1147,7 +1164,11 @@ int launch_query(SearchArgs a, cudaStream_t st) {
   }
   if (rc == GGNN_OK) {
     b.pilot = 0;
-    rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS);
+    static const int occ = [] {
+      const char* e = getenv("GGNN_OCC_CAP");
+      return e ? atoi(e) : 0;
+    }();
+    rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS, occ);
   }
   cudaFreeAsync(buf, st);
   return rc;

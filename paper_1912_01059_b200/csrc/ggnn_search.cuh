@@ -6,7 +6,9 @@
 // match the reference bit for bit.  The cache lives in
 // shared memory, one private region per warp:
 //
-//   rk[cap], rid[cap], rvis[cap]  the sorted ring (best-list + priority queue)
+//   rk[cap], rid[cap], rvis[cap]  the sorted ring (best-list + priority queue);
+//                                 uint32 keys: one u64 word per entry,
+//                                 key << 32 | id << 1 | visited
 //   vring[vsz]                    the visited ring (FIFO of expanded ids)
 //   ht[H]                         exact refcount table over ring u vring
 //   crow/cid/ckey[32]             per-step candidate scratch
@@ -65,14 +67,15 @@ __host__ __device__ inline bool vring_local(int vsz) { return vsz <= 32 * VR_SLO
 
 // Lay out one warp's shared region (offsets into c, computed once on the
 // host so the kernels address every array as base + constant) and return its
-// byte size: ring keys + ids (packed u64 words for 4-byte keys), visited
-// flags (padded for 4-byte scans), the shared visited ring when it is too
+// byte size: ring keys + ids (packed u64 words for 4-byte keys, whose low
+// bit is the visited flag), visited flags otherwise (padded for 4-byte
+// scans), the shared visited ring when it is too
 // large for the lanes, the refcount table, candidate rows / ids / keys and
 // the query.
 inline size_t set_layout(SearchCfg& c, int64_t d, int qelem, int keysize) {
   size_t b = align16((size_t)c.cap * keysize) + align16((size_t)c.cap * 4);
   c.o_rvis = (uint32_t)b;
-  b += align16((size_t)((c.cap + 127) / 128) * 128);
+  if (keysize != 4) b += align16((size_t)((c.cap + 127) / 128) * 128);
   c.o_vring = (uint32_t)b;
   if (!vring_local(c.vsz)) b += align16((size_t)c.vsz * 4);
   c.o_ht = (uint32_t)b;
@@ -95,6 +98,14 @@ inline int table_log2(int cap, int vsz) {
   while ((1 << lg) < need) ++lg;
   return lg;
 }
+
+// Refcount-table purge threshold in sixteenths of the table: linear probing
+// counts tombstones as occupied, so a miss costs ~(1 + 1/(1-a)^2)/2 probes at
+// occupancy a; purging earlier trades rebuilds for shorter probe chains.
+#ifndef GGNN_HT_FILL
+#define GGNN_HT_FILL 12
+#endif
+constexpr int HT_FILL = GGNN_HT_FILL;
 
 // 128-byte lines of each neighbour row prefetched into L1 at the start of an
 // expansion (0 disables; rows longer than this are only partly prefetched)
@@ -173,8 +184,17 @@ struct WarpSearch {
     else return rk[i];
   }
   __device__ __forceinline__ int ring_id(int i) const {
-    if constexpr (PACK) return (int)(uint32_t)re[i];
+    if constexpr (PACK) return (int)((uint32_t)re[i] >> 1);
     else return rid[i];
+  }
+  // packed ring word: key << 32 | id << 1 | visited.  The flag below the id
+  // keeps the (key, id) order of the words (ids are distinct, < 2^31).
+  static __device__ __forceinline__ uint64_t ring_word(uint32_t key, int id) {
+    return ((uint64_t)key << 32) | ((uint64_t)(uint32_t)id << 1);
+  }
+  __device__ __forceinline__ bool ring_vis(int i) const {
+    if constexpr (PACK) return (reinterpret_cast<const uint32_t*>(re)[2 * i] & 1u) != 0u;
+    else return rvis[i] != 0;
   }
 
   __device__ void carve(uint8_t* base) {
@@ -198,7 +218,7 @@ struct WarpSearch {
   __device__ void reset() {
     ht.clear();
     L = vlen = vpos = used = 0;
-    rebuild_at = (int)((ht.mask + 1) * 3 / 4);
+    rebuild_at = (int)((ht.mask + 1) * HT_FILL / 16);
     pf_node = -1;
     pf_nb = -1;
     next_head = -2;
@@ -229,10 +249,11 @@ struct WarpSearch {
     for (int i = lane; i < L; i += 32) u += ht.add_one((uint32_t)ring_id(i));
     for (int i = lane; i < vlen; i += 32) u += ht.add_one((uint32_t)(vring ? vring[i] : vr[i >> 5]));
     used = warp_sum(u);
-    // next purge once tombstones fill an eighth of the table, never so late
-    // that fewer than 40 slots stay empty (one merge adds at most 32)
+    // next purge once the occupied slots (live + tombstones) pass HT_FILL / 16
+    // of the table or tombstones fill an eighth of it, never so late that
+    // fewer than 40 slots stay empty (one merge adds at most 32)
     const int size = (int)ht.mask + 1;
-    rebuild_at = min(max(size * 3 / 4, used + size / 8), size - 40);
+    rebuild_at = min(max(size * HT_FILL / 16, used + size / 8), size - 40);
     __syncwarp();
   }
 
@@ -242,6 +263,15 @@ struct WarpSearch {
   // first unvisited ring position >= start (start a multiple of 4 or not), -1 if none
   __device__ int head_from(int start) const {
     const int lane = lane_id();
+    if constexpr (PACK) {
+      const uint32_t* lo = reinterpret_cast<const uint32_t*>(re);  // low words: id << 1 | visited
+      for (int base = start; base < L; base += 32) {
+        const int p = base + lane;
+        const unsigned bal = __ballot_sync(FULL, p < L && (lo[2 * p] & 1u) == 0u);
+        if (bal) return base + __ffs(bal) - 1;
+      }
+      return -1;
+    }
     for (int base = start & ~3; base < L; base += 128) {
       const int p0 = base + 4 * lane;
       const uint32_t w = *reinterpret_cast<const uint32_t*>(rvis + p0);
@@ -298,7 +328,7 @@ struct WarpSearch {
     const bool in = lane < E;
     const int r = L - 1 - lane;
     const int t = in ? ring_id(r) : -1;
-    const bool vis = in && rvis[r] != 0;
+    const bool vis = in && ring_vis(r);
     const bool gone = in && !vis;
     if (gone) ht.tomb_lane((uint32_t)t);
     forgotten += __popc(__ballot_sync(FULL, gone));
@@ -321,7 +351,7 @@ struct WarpSearch {
     if (lane < m) {
       int lo = 0, hi = L;
       if constexpr (PACK) {
-        const uint64_t pk = pack_ki((uint32_t)key, id);
+        const uint64_t pk = ring_word((uint32_t)key, id);
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
           if (re[mid] <= pk)
@@ -370,10 +400,8 @@ struct WarpSearch {
       const int o = hi - 32 + lane;
       if constexpr (PACK) {
         const uint64_t ee = re[o - madm];
-        const uint8_t vv = rvis[o - madm];
         __syncwarp();
         re[o] = ee;
-        rvis[o] = vv;
       } else {
         const Key kk = rk[o - madm];
         const int ii = rid[o - madm];
@@ -394,18 +422,10 @@ struct WarpSearch {
       const int below = __popc(__ballot_sync(FULL, ok && p < cb)) + __popc(cmask & lanemask_lt());
       const bool is_c = (cmask >> lane) & 1u;
       if constexpr (PACK) {
-        uint64_t ee = __shfl_sync(FULL, pack_ki((uint32_t)key, id), below & 31);
-        uint8_t vv = 0;
-        if (act && !is_c) {
-          const int r = o - below;
-          ee = re[r];
-          vv = rvis[r];
-        }
+        uint64_t ee = __shfl_sync(FULL, ring_word((uint32_t)key, id), below & 31);
+        if (act && !is_c) ee = re[o - below];
         __syncwarp();
-        if (act) {
-          re[o] = ee;
-          rvis[o] = vv;
-        }
+        if (act) re[o] = ee;
       } else {
         const Key ck = KO::shfl(key, below & 31);
         const int ci = __shfl_sync(FULL, id, below & 31);
@@ -486,7 +506,10 @@ struct WarpSearch {
     }
     const int node = ring_id(pos);
     __syncwarp();
-    if (lane == 0) rvis[pos] = 1;
+    if (lane == 0) {
+      if constexpr (PACK) reinterpret_cast<uint32_t*>(re)[2 * pos] |= 1u;
+      else rvis[pos] = 1;
+    }
     vring_push(node);
     ht.inc((uint32_t)node);
 
@@ -639,7 +662,7 @@ struct WarpSearch {
     if (L >= c.k_out)
       thr = __dadd_rn(KO::to_d(ring_key(c.k_out - 1)), __dmul_rn(c.tau, fmin(dmax, KO::to_d(ring_key(0)))));
     int n = 0;
-    for (int i = lane_id(); i < L; i += 32) n += (!rvis[i] && KO::to_d(ring_key(i)) <= thr) ? 1 : 0;
+    for (int i = lane_id(); i < L; i += 32) n += (!ring_vis(i) && KO::to_d(ring_key(i)) <= thr) ? 1 : 0;
     return warp_sum(n);
   }
 
