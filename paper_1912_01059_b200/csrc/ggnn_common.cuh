@@ -304,9 +304,15 @@ __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const 
 #ifndef GGNN_DISTS_V2
 #define GGNN_DISTS_V2 1
 #endif
-template <int UNR>
+// `hook` (warp-collective, independent of the distances) runs once while the
+// first row gathers are in flight: the caller's bookkeeping leaves the
+// dependent chain of the step.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <int UNR, typename Hook>
 __device__ __forceinline__ void dists_u8_lp8(const uint8_t* X, int64_t d, const uint8_t* qs, const int* rows, int cnt,
-                                             uint32_t* kout) {
+                                             uint32_t* kout, Hook& hook) {
   constexpr int LPR = 8, RPP = 32 / LPR;
   const int lane = lane_id();
   const int sub = lane & (LPR - 1);
@@ -323,6 +329,7 @@ __device__ __forceinline__ void dists_u8_lp8(const uint8_t* X, int64_t d, const 
       v[u] = make_uint4(0u, 0u, 0u, 0u);
       if (mine && ci < cnt) v[u] = __ldg(X4 + (size_t)(uint32_t)rows[ci] * nch);
     }
+    if (base == 0) hook();
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const uint32_t t = group_reduce<LPR, uint32_t>(part_u8(v[u], qv));
@@ -389,12 +396,18 @@ __device__ __forceinline__ void warp_dists(const TX* X, int64_t d, const TQ* qs,
 #ifndef GGNN_U8_UNR
 #define GGNN_U8_UNR 4  // row groups in flight for 128-byte uint8 rows (dists_u8_lp8: 16 rows; 3 and 6 measured slower)
 #endif
-template <typename TX, typename TQ, int LP>
+template <typename TX, typename TQ, int LP, typename Hook = NoHook>
 __device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* qs, const int* rows, int cnt,
-                                             typename VecTraits<TX, TQ>::Key* kout, int lpr) {
+                                             typename VecTraits<TX, TQ>::Key* kout, int lpr, Hook hook = Hook()) {
+  if constexpr (LP == 8 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value &&
+                GGNN_DISTS_V2 != 0) {
+    if (cnt > 0) dists_u8_lp8<GGNN_U8_UNR>(X, d, qs, rows, cnt, kout, hook);
+    else hook();
+    return;
+  }
+  hook();
   if constexpr (LP == 8 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
-    if constexpr (GGNN_DISTS_V2 != 0) dists_u8_lp8<GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
-    else dists_u8_vec<8, GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
+    dists_u8_vec<8, GGNN_U8_UNR>(X, d, qs, rows, cnt, kout);
   } else if constexpr (LP == 32 && std::is_same<TX, uint8_t>::value && std::is_same<TQ, uint8_t>::value) {
     dists_u8_vec<32, 4>(X, d, qs, rows, cnt, kout);
   } else if constexpr (LP == 8 && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {

@@ -511,7 +511,9 @@ struct WarpSearch {
       else rvis[pos] = 1;
     }
     vring_push(node);
-    ht.inc((uint32_t)node);
+    // ht.inc(node) and the scan for the next unvisited entry do not depend on
+    // this step's candidates: they run while the row gathers are in flight
+    // (node's count only matters to later lookups; it is in the ring already)
 
     int nb = -1;
     if (node == pf_node) {
@@ -551,7 +553,11 @@ struct WarpSearch {
         cid[ci] = nb;
       }
       __syncwarp();
-      warp_dists_t<TX, TQ, LP>(X, d, qs, crow, nc, ckey, lpr);
+      int q = -1;
+      warp_dists_t<TX, TQ, LP>(X, d, qs, crow, nc, ckey, lpr, [&]() {
+        ht.inc((uint32_t)node);
+        q = head_from(pos + 1);
+      });
       __syncwarp();
       Key key = KO::max_key();
       int id = INT_MAX;
@@ -620,12 +626,12 @@ struct WarpSearch {
         if (target >= 0) found = __any_sync(FULL, adm && id == target);
       }
       // predict the next expansion -- the smaller of the next unvisited ring
-      // entry and the best admitted candidate -- and load its adjacency row
+      // entry q and the best admitted candidate -- and load its adjacency row
       // while the merge runs (checked against the real head next step)
-      const int q = head_from(pos + 1);
       if (!found) prefetch_next(q, m > 0, KO::shfl(key, 0), __shfl_sync(FULL, id, 0));
       next_head = m ? merge(key, id, m, q) : q;
     } else {
+      ht.inc((uint32_t)node);
       const int q = head_from(pos + 1);
       prefetch_next(q, false, KO::max_key(), INT_MAX);
       next_head = q;
