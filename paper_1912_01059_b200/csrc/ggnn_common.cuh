@@ -166,10 +166,6 @@ __device__ __forceinline__ float part_f32_sp(const float4 a, const float* q) {
 #ifndef GGNN_F32_UNR
 #define GGNN_F32_UNR 4  // float rows in flight per lane group
 #endif
-#ifndef GGNN_F32_CUNR
-#define GGNN_F32_CUNR 1  // unroll of the per-row chunk loop (long float rows)
-#endif
-constexpr int F32_CUNR = GGNN_F32_CUNR;  // (#pragma unroll does not expand macros)
 
 __device__ __forceinline__ double part_f32(const float4 a, const float* q) {
   double d0 = (double)a.x - (double)q[0], d1 = (double)a.y - (double)q[1];
@@ -203,9 +199,16 @@ __device__ __forceinline__ Acc group_reduce(Acc v) {
   return v;
 }
 
-template <int LPR, int UNR>
+// `hook` (warp-collective, independent of the distances) runs once while the
+// first row gathers are in flight: the caller's bookkeeping leaves the
+// dependent chain of the step.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <int LPR, int UNR, typename Hook = NoHook>
 __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const float* qs, const int* rows, int cnt,
-                                              double* kout) {
+                                              double* kout, Hook&& hook = Hook()) {
   const int lane = lane_id();
   const int nch = (int)(d >> 2);
   constexpr int RPP = 32 / LPR;
@@ -224,12 +227,19 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
     float accf[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) accf[u] = 0.0f;
-#pragma unroll F32_CUNR
-    for (int c = sub; c < nch; c += LPR) {
-      float4 v[UNR];
+    // first chunk's loads, then the hook (every lane, also those without a
+    // chunk: it is warp-collective), then the chunk loop (LPR < 32: at most
+    // one chunk per lane, see dists_u8_vec)
+    int c = sub;
+    bool have = c < nch;
+    float4 v[UNR];
+    if (have) {
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
         if (rp[u]) v[u] = __ldg(rp[u] + c);
+    }
+    if (base == 0) hook();
+    while (have) {
       const float* qc = qs + 4 * c;
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
@@ -237,7 +247,13 @@ __device__ __forceinline__ void dists_f32_vec(const float* X, int64_t d, const f
         if constexpr (GGNN_F32_PARTIALS) accf[u] += part_f32_sp(v[u], qc);
         else acc[u] += part_f32(v[u], qc);
       }
-      if constexpr (LPR < 32) break;  // at most one chunk per lane (see dists_u8_vec)
+      c += LPR;
+      have = LPR == 32 && c < nch;
+      if (have) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          if (rp[u]) v[u] = __ldg(rp[u] + c);
+      }
     }
     if constexpr (GGNN_F32_PARTIALS) {
 #pragma unroll
@@ -304,12 +320,6 @@ __device__ __forceinline__ void dists_u8_vec(const uint8_t* X, int64_t d, const 
 #ifndef GGNN_DISTS_V2
 #define GGNN_DISTS_V2 1
 #endif
-// `hook` (warp-collective, independent of the distances) runs once while the
-// first row gathers are in flight: the caller's bookkeeping leaves the
-// dependent chain of the step.
-struct NoHook {
-  __device__ __forceinline__ void operator()() const {}
-};
 template <int UNR, typename Hook>
 __device__ __forceinline__ void dists_u8_lp8(const uint8_t* X, int64_t d, const uint8_t* qs, const int* rows, int cnt,
                                              uint32_t* kout, Hook& hook) {
@@ -403,6 +413,16 @@ __device__ __forceinline__ void warp_dists_t(const TX* X, int64_t d, const TQ* q
                 GGNN_DISTS_V2 != 0) {
     if (cnt > 0) dists_u8_lp8<GGNN_U8_UNR>(X, d, qs, rows, cnt, kout, hook);
     else hook();
+    return;
+  }
+  if constexpr ((LP == 8 || LP == 32) && std::is_same<TX, float>::value && std::is_same<TQ, float>::value) {
+    // (every lane owns a chunk of a float row: d / 4 >= LP, see choose_lpr)
+    if (cnt > 0) {
+      if constexpr (LP == 8) dists_f32_vec<8, 4>(X, d, qs, rows, cnt, kout, hook);
+      else dists_f32_vec<32, GGNN_F32_UNR>(X, d, qs, rows, cnt, kout, hook);
+    } else {
+      hook();
+    }
     return;
   }
   hook();

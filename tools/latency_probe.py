@@ -13,7 +13,11 @@ from paper_1912_01059_b200 import _native as N  # noqa: E402
 from paper_1912_01059_b200.device import device_hierarchy  # noqa: E402
 from paper_1912_01059_b200.synthetic import make_latent16  # noqa: E402
 
-base, Q = make_latent16(n=1_000_000, d=128, m=10_000, seed=1234)
+import os  # noqa: E402
+
+# FLOAT=1: the sift1m-f32 workload (non-integer float32 rows); D: dimension
+base, Q = make_latent16(n=1_000_000, d=int(os.environ.get("D", 128)), m=10_000, seed=1234,
+                        as_float=os.environ.get("FLOAT") == "1")
 import time  # noqa: E402
 
 ga.build(ga.Dataset(base[:50_000]), ga.BuildConfig(seed=7))  # warm-up (module loading, allocator growth)
