@@ -331,20 +331,53 @@ __device__ __forceinline__ void dists_u8_lp8(const uint8_t* X, int64_t d, const 
   const bool mine = (uint32_t)sub < nch;
   const uint4* X4 = reinterpret_cast<const uint4*>(X) + sub;
   const uint4 qv = mine ? reinterpret_cast<const uint4*>(qs)[sub] : make_uint4(0u, 0u, 0u, 0u);
-  for (int base = 0; base < cnt; base += RPP * UNR) {
-    uint4 v[UNR];
+  if constexpr (UNR == 4) {
+    // group g owns candidates base + 4g .. base + 4g + 3 (one 16-byte read of
+    // their rows; rows / kout are 16-byte aligned 32-entry arrays), and the
+    // four sums are reduced transposed: 4 shuffles instead of 12, after which
+    // lane sub (even) of the group holds the sum of candidate 2 (sub & 4) / 4 + (sub & 2) / 2
+    for (int base = 0; base < cnt; base += 16) {
+      const int c0 = base + 4 * grp;
+      const int4 r4 = *reinterpret_cast<const int4*>(rows + c0);
+      const int rr[4] = {r4.x, r4.y, r4.z, r4.w};
+      uint4 v[4];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int ci = base + u * RPP + grp;
-      v[u] = make_uint4(0u, 0u, 0u, 0u);
-      if (mine && ci < cnt) v[u] = __ldg(X4 + (size_t)(uint32_t)rows[ci] * nch);
+      for (int u = 0; u < 4; ++u) {
+        v[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (mine && c0 + u < cnt) v[u] = __ldg(X4 + (size_t)(uint32_t)rr[u] * nch);
+      }
+      if (base == 0) hook();
+      uint32_t a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = part_u8(v[u], qv);
+      const bool b2 = (sub & 4) != 0, b1 = (sub & 2) != 0;
+      uint32_t x0 = b2 ? a[2] : a[0], x1 = b2 ? a[3] : a[1];
+      const uint32_t y0 = b2 ? a[0] : a[2], y1 = b2 ? a[1] : a[3];
+      x0 += __shfl_xor_sync(FULL, y0, 4);
+      x1 += __shfl_xor_sync(FULL, y1, 4);
+      uint32_t z = b1 ? x1 : x0;
+      const uint32_t w = b1 ? x0 : x1;
+      z += __shfl_xor_sync(FULL, w, 2);
+      z += __shfl_xor_sync(FULL, z, 1);
+      const int ci = c0 + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+      if ((sub & 1) == 0 && ci < cnt) kout[ci] = z;
     }
-    if (base == 0) hook();
+  } else {
+    for (int base = 0; base < cnt; base += RPP * UNR) {
+      uint4 v[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const uint32_t t = group_reduce<LPR, uint32_t>(part_u8(v[u], qv));
-      const int ci = base + u * RPP + grp;
-      if (sub == 0 && ci < cnt) kout[ci] = t;
+      for (int u = 0; u < UNR; ++u) {
+        const int ci = base + u * RPP + grp;
+        v[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (mine && ci < cnt) v[u] = __ldg(X4 + (size_t)(uint32_t)rows[ci] * nch);
+      }
+      if (base == 0) hook();
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint32_t t = group_reduce<LPR, uint32_t>(part_u8(v[u], qv));
+        const int ci = base + u * RPP + grp;
+        if (sub == 0 && ci < cnt) kout[ci] = t;
+      }
     }
   }
 }
