@@ -585,7 +585,7 @@ struct WarpSearch {
           uint32_t* ck = reinterpret_cast<uint32_t*>(ckey);
           if (lane >= nc && lane < ((nc + 3) & ~3)) ck[lane] = 0x7fffffffu;  // never below a real key
           __syncwarp();
-          int rank = 0, eq = 0;
+          int rank = 0;
           const uint32_t kk = (uint32_t)key;
           if (adm) {
             const uint4* k4 = reinterpret_cast<const uint4*>(ck);
@@ -593,18 +593,26 @@ struct WarpSearch {
               const uint4 w = k4[j >> 2];
               rank += (int)((w.x - kk) >> 31) + (int)((w.y - kk) >> 31) + (int)((w.z - kk) >> 31) +
                       (int)((w.w - kk) >> 31);
-              eq += (int)(w.x == kk) + (int)(w.y == kk) + (int)(w.z == kk) + (int)(w.w == kk);
             }
-          }
-          // equal keys (only admitted ones can equal an admitted key): the
-          // smaller id first, the (key, id) order of the ring; eq counts self
-          if (adm && eq > 1) {
-            for (int j = 0; j < nc; ++j) rank += (ck[j] == kk && cid[j] < id) ? 1 : 0;
           }
           __syncwarp();
           uint64_t* sc = reinterpret_cast<uint64_t*>(crow);  // crow + cid: 32 words
-          if (adm) sc[rank] = pack_ki((uint32_t)key, id);
+          const uint64_t mine = pack_ki(kk, id);
+          if (adm) sc[rank] = mine;
           __syncwarp();
+          // equal keys (only admitted ones can equal an admitted key) share a
+          // count and collide in sc: rank them by id, the (key, id) order of
+          // the ring (rare; candidate j's key / id sit in lane j)
+          if (__any_sync(FULL, adm && sc[rank] != mine)) {
+            for (int j = 0; j < nc; ++j) {
+              const uint32_t kj = __shfl_sync(FULL, kk, j);
+              const int ij = __shfl_sync(FULL, id, j);
+              rank += (adm && kj == kk && ij < id) ? 1 : 0;
+            }
+            __syncwarp();
+            if (adm) sc[rank] = mine;
+            __syncwarp();
+          }
           if (lane < m) {
             const uint64_t v = sc[lane];
             key = (Key)(v >> 32);
