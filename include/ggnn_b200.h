@@ -138,6 +138,11 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
  * Process-wide. */
 int ggnn_query_schedule(long long pilot_steps, double min_waves);
 
+/* Number of kernels this library has launched in this process (all entry
+ * points; no reference counterpart): the bench reads it around its timed
+ * region to report gpu_launches. */
+unsigned long long ggnn_kernel_launches(void);
+
 /* Replaces: query (search.py:115-137) for a batch, like ggnn_query_batch,
  * over float32 queries that are still being uploaded (the
  * host-to-host path overlaps the upload with the search): rows

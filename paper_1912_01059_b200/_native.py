@@ -79,6 +79,7 @@ _SIGS = {
     "ggnn_tc_timeouts": [],
     "ggnn_search_accounting": [P],
     "ggnn_query_schedule": [I64, F64],
+    "ggnn_kernel_launches": [],
     "ggnn_merge_descent": [P, P, I32, I32, I32, P, I64, P, I32, I32, P, P, P, P, P],
     "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_merge_rows_range": [I64, I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
@@ -107,7 +108,7 @@ _SIGS = {
 _RESTYPES = {"ggnn_last_error": ctypes.c_char_p, "ggnn_search_workspace_bytes": ctypes.c_size_t,
              "ggnn_layer_stats_scratch_bytes": ctypes.c_size_t, "ggnn_shard_block_bytes": ctypes.c_size_t,
              "ggnn_shard_block_dists_offset": ctypes.c_size_t, "ggnn_shard_block_counters_offset": ctypes.c_size_t,
-             "ggnn_p2p_bytes": ctypes.c_size_t}
+             "ggnn_p2p_bytes": ctypes.c_size_t, "ggnn_kernel_launches": ctypes.c_ulonglong}
 # entry points added by later translation units register themselves here
 EXTRA_SIGS: dict = {}
 

@@ -301,6 +301,7 @@ int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_i
   GGNN_CUDA_TRY(cudaMemsetAsync(blocks, 0, bb * halves * splits, st));
   const uint8_t* Xd = static_cast<const uint8_t*>(X->d_data);
   sqnorm_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Xd, n, X->d, xnorm);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   BfArgs a;
   a.X = Xd;
@@ -322,14 +323,17 @@ int bf_topk_tc(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d_i
   if (halves == 2) {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bf_tc_kernel<2><<<(unsigned)(qtiles * splits), 256, smem, st>>>(a);
+    count_launch();
     GGNN_LAUNCH_CHECK();
     rc = ggnn_shard_merge(blocks, (int32_t)(2 * splits), m, k, k, d_ids, d_dists, nullptr, st);
   } else {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bf_tc_kernel<1><<<(unsigned)(qtiles * splits), 128, smem, st>>>(a);
+    count_launch();
     GGNN_LAUNCH_CHECK();
     merge_lists_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(blocks, bb, a.dists_off, (int)splits, m, k,
                                                                      d_ids, d_dists);
+    count_launch();
     GGNN_LAUNCH_CHECK();
   }
   cudaFreeAsync(blocks, st);

@@ -384,10 +384,14 @@ int bf_topk_tf32(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d
   GGNN_CUDA_TRY(cudaMemsetAsync(xmax, 0, 64, st));
   col_sum_kernel<<<(unsigned)std::min<int64_t>(std::max(di.sm_count, 1) * 8, std::max<int64_t>(1, n / 64)), 256, 0,
                    st>>>(Xd, n, d, sums);
+  count_launch();
   mean_kernel<<<(d + 255) / 256, 256, 0, st>>>(sums, n, d, mu);
+  count_launch();
   row_norm_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(Xd, n, d, mu, xn, xmax);
+  count_launch();
   const float* Qf = static_cast<const float*>(Q->d_data);
   query_norm_kernel<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(Xd, Qf, Q->d_rows, m, d, mu, qn);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   Tf32Args a;
   a.X = Xd;
@@ -406,8 +410,10 @@ int bf_topk_tf32(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d
   const size_t smem = tf32_smem();
   GGNN_CUDA_TRY(cudaFuncSetAttribute(bf_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   bf_tf32_kernel<<<(unsigned)(qtiles * splits), TB_M, smem, st>>>(a);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   bf_tf32_finalize<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(a, Qf, qn, xmax, k, d_ids, d_dists, flag, nflag);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   // the one host synchronisation of this path: how many queries need the
   // CUDA-core scan (almost always none)
@@ -418,6 +424,7 @@ int bf_topk_tf32(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d
   if (nf > 0) {  // the few queries whose candidate lists may be cut: CUDA-core scan
     GGNN_CUDA_TRY(cudaMemsetAsync(nflag, 0, 4, st));
     flagged_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(flag, m, sel, nflag);
+    count_launch();
     float* qsub = nullptr;
     int32_t* ids2 = nullptr;
     double* d2 = nullptr;
@@ -425,8 +432,12 @@ int bf_topk_tf32(const ggnn_vectors* X, const ggnn_queries* Q, int k, int32_t* d
     GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ids2), (size_t)nf * k * 4, st));
     GGNN_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d2), (size_t)nf * k * 8, st));
     gather_rows_kernel<<<(unsigned)nf, 128, 0, st>>>(Xd, Qf, Q->d_rows, sel, nf, d, qsub);
+    count_launch();
     rc = topk_scan_subset(X, qsub, nf, k, ids2, d2, st);
-    if (rc == GGNN_OK) scatter_rows_kernel<<<(unsigned)nf, 32, 0, st>>>(sel, nf, k, ids2, d2, d_ids, d_dists);
+    if (rc == GGNN_OK) {
+      scatter_rows_kernel<<<(unsigned)nf, 32, 0, st>>>(sel, nf, k, ids2, d2, d_ids, d_dists);
+      count_launch();
+    }
     cudaFreeAsync(qsub, st);
     cudaFreeAsync(ids2, st);
     cudaFreeAsync(d2, st);

@@ -815,10 +815,12 @@ static int leaf_knn_impl(const ggnn_vectors* X, const int32_t* d_nodes, const in
       GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
       leaf_knn_tc_kernel<64><<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+      count_launch();
     } else {
       GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
       leaf_knn_tc_kernel<128><<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+      count_launch();
     }
     GGNN_LAUNCH_CHECK();
     return GGNN_OK;
@@ -830,6 +832,7 @@ static int leaf_knn_impl(const ggnn_vectors* X, const int32_t* d_nodes, const in
     const int64_t grid = std::min<int64_t>(nbatches, (int64_t)std::max(di.sm_count, 1) * per_sm);
     GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     leaf_knn_tf32_kernel<<<(unsigned)grid, TC_ROWS, smem, st>>>(a, nbatches);
+    count_launch();
     GGNN_LAUNCH_CHECK();
     return GGNN_OK;
   }
@@ -845,9 +848,11 @@ static int leaf_knn_impl(const ggnn_vectors* X, const int32_t* d_nodes, const in
   if (X->dtype == GGNN_U8) {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     leaf_knn_kernel<uint8_t><<<(unsigned)nbatches, 256, smem, st>>>(a);
+    count_launch();
   } else {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(leaf_knn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     leaf_knn_kernel<float><<<(unsigned)nbatches, 256, smem, st>>>(a);
+    count_launch();
   }
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
@@ -898,6 +903,7 @@ int ggnn_merge_rows_range(int64_t node_begin, int64_t count, int32_t k, int32_t 
   MergeArgs a{count, node_begin, k, k_nn, d_adj, d_nnd, d_sym_count, d_dnn1, d_hit_ids, d_hit_dists, hits_per_node,
               d_resc_ids, d_resc_dists, d_changed};
   merge_rows_kernel<<<(unsigned)((count + 7) / 8), 256, 0, as_stream(stream)>>>(a);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -917,10 +923,14 @@ int ggnn_sym_claim_round(const int32_t* d_req, int64_t nreq, int32_t n_fallback,
   cudaStream_t st = as_stream(stream);
   const unsigned grid = (unsigned)((nreq + 255) / 256);
   claim_first_kernel<<<grid, 256, 0, st>>>(a);
+  count_launch();
   claim_propose_kernel<<<grid, 256, 0, st>>>(a);
+  count_launch();
   claim_accept_kernel<<<grid, 256, 0, st>>>(a);
+  count_launch();
   GGNN_CUDA_TRY(cudaMemsetAsync(d_pending, 0, sizeof(int32_t), st));
   claim_reset_kernel<<<grid, 256, 0, st>>>(a);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -932,6 +942,7 @@ int ggnn_sym_compact(const int32_t* d_stage, const int32_t* d_idx_in, int64_t n_
   GGNN_CUDA_TRY(cudaMemsetAsync(d_n_out, 0, sizeof(int32_t), st));
   if (n_in == 0) return GGNN_OK;
   compact_open_kernel<<<(unsigned)((n_in + 255) / 256), 256, 0, st>>>(d_stage, d_idx_in, n_in, d_idx_out, d_n_out);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -940,7 +951,9 @@ int ggnn_layer_stats(const double* d_values, int64_t n, double* d_scratch, doubl
   GGNN_CHECK_ARG(d_values && d_scratch && d_out && n >= 0, "invalid arguments");
   cudaStream_t st = as_stream(stream);
   stats_partial_kernel<<<STATS_BLOCKS, 256, 0, st>>>(d_values, n, d_scratch);
+  count_launch();
   stats_final_kernel<<<1, 32, 0, st>>>(d_scratch, STATS_BLOCKS, d_out);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }

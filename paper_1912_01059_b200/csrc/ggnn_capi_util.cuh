@@ -28,6 +28,9 @@ void set_error(const char* fmt, ...);
 
 #define GGNN_LAUNCH_CHECK() GGNN_CUDA_TRY(cudaGetLastError())
 
+// process-wide count of the kernels this library launched (ggnn_kernel_launches)
+void count_launch(int n = 1);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 struct DevInfo {

@@ -584,6 +584,23 @@ struct RefTable {
     }
     __syncwarp();
   }
+  // increment of a key known to be present: one lane probes (the key sits
+  // within a slot or two of its home), no warp-wide ballots
+  __device__ __forceinline__ void inc_present(uint32_t key) {
+    if (lane_id() == 0) {
+      uint32_t s = home(key);
+      for (;;) {
+        const uint32_t v = t[s];
+        if (v != TOMB && v != EMPTY && (v & KMASK) == key) {
+          t[s] = v + ONE;
+          break;
+        }
+        if (v == EMPTY) break;  // absent: nothing to count (as inc)
+        s = (s + 1) & mask;
+      }
+    }
+    __syncwarp();
+  }
   __device__ __forceinline__ void tomb(uint32_t key) {
     int s = find_slot(key);
     __syncwarp();

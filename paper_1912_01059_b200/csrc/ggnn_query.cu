@@ -5,6 +5,7 @@
 // private shared-memory region (ring + visited ring + refcount table + query).
 // Every search is independent, so the grid is simply ceil(m / W) CTAs and the
 // hardware block scheduler balances the (very uneven) per-query work.
+#include <atomic>
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -48,6 +49,9 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
   g_err = buf;
 }
+
+std::atomic<unsigned long long> g_kernel_launches{0};
+void count_launch(int n) { g_kernel_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 DevInfo dev_info() {
   static DevInfo info{0, 0, 0};
@@ -1035,6 +1039,7 @@ int launch_items(Kern kern, Args a, int64_t items, size_t region, cudaStream_t s
     a.chunk = (int)std::max<int64_t>(1, std::min<int64_t>(GGNN_WORK_CHUNK, items / (grid * W * 16)));
   }
   kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -1146,6 +1151,7 @@ int launch_query(SearchArgs a, cudaStream_t st) {
   int rc = launch_warps(qk, a, a.m, a.region, st);
   if (rc == GGNN_OK) {
     park_order_kernel<<<1, PARK_BUCKETS, 0, st>>>(a.park_key, a.m, order, count);
+    count_launch();
     rc = cudaGetLastError() == cudaSuccess ? GGNN_OK : GGNN_E_CUDA;
     if (rc) set_error("park_order_kernel launch failed");
   }
@@ -1158,6 +1164,7 @@ int launch_query(SearchArgs a, cudaStream_t st) {
     rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS);
     if (rc == GGNN_OK) {
       park_order_kernel<<<1, PARK_BUCKETS, 0, st>>>(a.park_key, a.m, order, count);
+      count_launch();
       rc = cudaGetLastError() == cudaSuccess ? GGNN_OK : GGNN_E_CUDA;
       if (rc) set_error("park_order_kernel launch failed");
     }
@@ -1322,6 +1329,7 @@ int count_distinct(const SearchArgs& a, cudaStream_t st) {
     GGNN_CUDA_TRY(cudaFuncSetAttribute(distinct_log_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   distinct_log_kernel<<<(unsigned)a.m, 256, smem, st>>>(a.ever, a.log_len, a.ever_size, a.counters, slots, g);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   if (g) GGNN_CUDA_TRY(cudaFreeAsync(g, st));
   return GGNN_OK;
@@ -1337,6 +1345,8 @@ int ggnn_search_accounting(unsigned long long* d_acc) {
   g_acc = d_acc;
   return GGNN_OK;
 }
+unsigned long long ggnn_kernel_launches(void) { return ggnn::g_kernel_launches.load(); }
+
 int ggnn_query_schedule(long long pilot_steps, double min_waves) {
   GGNN_CHECK_ARG(min_waves >= 0.0, "min_waves must be >= 0");
   g_pilot = pilot_steps;
@@ -1377,6 +1387,7 @@ int ggnn_rows_unique(const int32_t* d_adj, int64_t node_count, int32_t k, int32_
   GGNN_CUDA_TRY(cudaMemcpyAsync(d_result, &one, sizeof(one), cudaMemcpyHostToDevice, st));
   if (node_count == 0) return GGNN_OK;
   rows_unique_kernel<<<(unsigned)((node_count + 7) / 8), 256, 0, st>>>(d_adj, node_count, k, d_result);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -1389,6 +1400,7 @@ int ggnn_sanitize_layer(const int32_t* d_adj, const int32_t* d_sym_count, int64_
   if (total == 0) return GGNN_OK;
   sanitize_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(d_adj, d_sym_count, node_count, k,
                                                                                    k_nn, d_out);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -1850,13 +1862,16 @@ int ggnn_squared_l2_many(const ggnn_vectors* X, const ggnn_queries* Q, const int
   if (X->dtype == GGNN_F32) {
     sqdist_kernel<float, float><<<grid, 128, 0, st>>>((const float*)X->d_data, X->d, (const float*)Q->d_data,
                                                       Q->d_rows, d_rows, per_query, total, d_out);
+    count_launch();
   } else if (qd == GGNN_U8) {
     sqdist_kernel<uint8_t, uint8_t><<<grid, 128, 0, st>>>((const uint8_t*)X->d_data, X->d,
                                                           (const uint8_t*)Q->d_data, Q->d_rows, d_rows, per_query,
                                                           total, d_out);
+    count_launch();
   } else {
     sqdist_kernel<uint8_t, float><<<grid, 128, 0, st>>>((const uint8_t*)X->d_data, X->d, (const float*)Q->d_data,
                                                         Q->d_rows, d_rows, per_query, total, d_out);
+    count_launch();
   }
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
@@ -1868,6 +1883,7 @@ int ggnn_f32_to_u8(const float* d_src, int64_t count, uint8_t* d_u8, int32_t* d_
   DevInfo di = dev_info();
   int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)std::max(di.sm_count, 1) * 8);
   f32_to_u8_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(d_src, count, d_u8, d_flag);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }

@@ -555,7 +555,7 @@ struct WarpSearch {
       __syncwarp();
       int q = -1;
       warp_dists_t<TX, TQ, LP>(X, d, qs, crow, nc, ckey, lpr, [&]() {
-        ht.inc((uint32_t)node);
+        ht.inc_present((uint32_t)node);
         q = head_from(pos + 1);
       });
       __syncwarp();
@@ -639,7 +639,7 @@ struct WarpSearch {
       if (!found) prefetch_next(q, m > 0, KO::shfl(key, 0), __shfl_sync(FULL, id, 0));
       next_head = m ? merge(key, id, m, q) : q;
     } else {
-      ht.inc((uint32_t)node);
+      ht.inc_present((uint32_t)node);
       const int q = head_from(pos + 1);
       prefetch_next(q, false, KO::max_key(), INT_MAX);
       next_head = q;

@@ -233,6 +233,7 @@ extern "C" int ggnn_p2p_signal(const ggnn_push* push, int64_t m, int32_t k, uint
     a.flags[g] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(push->d_peers[g]) + (size_t)push->parity * half +
                                              (size_t)push->nranks * block_bytes(m, k)) + push->rank;
   p2p_signal_kernel<<<1, 32, 0, as_stream(stream)>>>(a);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -250,6 +251,7 @@ extern "C" int ggnn_shard_globalize(int32_t* d_ids, int64_t count, const int32_t
   const int64_t want = (count + threads - 1) / threads;
   const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
   globalize_kernel<<<blocks, threads, 0, as_stream(stream)>>>(d_ids, count, d_gid_of_local, size);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
@@ -301,6 +303,7 @@ static int shard_merge_impl(const void* d_blocks, int32_t G, int64_t m, int32_t 
   const int wpb = 8;
   const int64_t blocks = (m + wpb - 1) / wpb;
   shard_merge_kernel<<<(unsigned)blocks, wpb * 32, 0, as_stream(stream)>>>(a);
+  count_launch();
   GGNN_LAUNCH_CHECK();
   return GGNN_OK;
 }
