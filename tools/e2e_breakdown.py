@@ -37,7 +37,7 @@ for it in range(30):
     search_s, copy_s = S._STREAMS[t.cuda.current_device()]
     st.epoch += 1
     st.epoch_pin[0] = st.epoch
-    params = S._params(cfg, S._flags(dv, False))
+    params = S._params(cfg, S._qflags(dh, False))
     e0, e1 = (t.cuda.Event(enable_timing=True) for _ in range(2))
     e0.record(search_s)
     T.append(time.perf_counter())
@@ -71,7 +71,7 @@ print(f"query_arrays end to end      {(time.perf_counter() - t0) / 20 * 1e3:7.3f
 st.chunk_flags.fill_(st.epoch)
 torch.cuda.synchronize()
 dq, qs = dh.vectors.queries(np.ascontiguousarray(Q))
-params = S._params(cfg, S._flags(dh.vectors, False))
+params = S._params(cfg, S._qflags(dh, False))
 
 
 def timed(fn, reps=10):
