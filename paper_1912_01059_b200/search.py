@@ -153,7 +153,30 @@ class _Staging:
         self.epoch_pin = t.zeros((1,), dtype=t.int32, pin_memory=True)
         self.status = N.empty((1,), t.int32)
         self.status_pin = t.empty((1,), dtype=t.int32, pin_memory=True)
+        # host-side views / device pointers of the fixed buffers, made once:
+        # the staged call's prelude delays the first kernel of every batch
+        self.epoch_np = self.epoch_pin.numpy()
+        self.status_np = self.status_pin.numpy()
+        self.ptrs = tuple(N.ptr(x) for x in (self.q_f32, self.chunk_flags, self.epoch_pin, self.ids, self.dists,
+                                            self.cnt, self.status, self.status_pin))
+        self.spare = None  # result arrays for the next call, allocated while a search runs
         return self
+
+    def results(self, m: int, k: int):
+        """Fresh page-locked result arrays (ids, dists, counters) for a call of
+        m queries: the spare set made during the previous call when it fits."""
+        t = N.torch()
+        sp, self.spare = self.spare, None
+        if sp is not None and sp[0].shape == (m, k):
+            return sp
+        return (t.empty((m, k), dtype=t.int32, pin_memory=True), t.empty((m, k), dtype=t.float64, pin_memory=True),
+                t.empty((m, 5), dtype=t.int32, pin_memory=True))
+
+    def prepare_spare(self, m: int, k: int):
+        t = N.torch()
+        self.spare = (t.empty((m, k), dtype=t.int32, pin_memory=True),
+                      t.empty((m, k), dtype=t.float64, pin_memory=True),
+                      t.empty((m, 5), dtype=t.int32, pin_memory=True))
 
 
 _STAGING: dict = {}
@@ -192,27 +215,27 @@ def _query_host_staged(dh, Q: np.ndarray, cfg: QueryConfig):
     search_s, copy_s = streams
     nchunks = max(1, min(_STAGED_CHUNKS, _STAGED_MAX_CHUNKS, m // 256))
     st.epoch = (st.epoch % 0x7FFFFFFF) + 1
-    st.epoch_pin[0] = st.epoch  # no copy of the previous call is pending (it synchronised)
+    st.epoch_np[0] = st.epoch  # no copy of the previous call is pending (it synchronised)
     params = _params(cfg, _qflags(dh, False))
     narrow = 1 if dv.exact_integers else 0
     # results land straight in fresh page-locked arrays that the caller keeps
     # (torch's caching host allocator makes these allocations cheap; the block
-    # returns to its cache when the arrays die): no host-side copy out
-    ids_h = t.empty((m, k), dtype=t.int32, pin_memory=True)
-    dists_h = t.empty((m, k), dtype=t.float64, pin_memory=True)
-    cnt_h = t.empty((m, 5), dtype=t.int32, pin_memory=True)
+    # returns to its cache when the arrays die): no host-side copy out.  The
+    # next call's set is allocated while this call's search runs.
+    ids_h, dists_h, cnt_h = st.results(m, k)
     for s_ in streams:
         s_.wait_stream(main)
+    q_f32, flags, epoch_pin, ids_d, dists_d, cnt_d, status_d, status_pin = st.ptrs
     N.call("ggnn_query_batch_host", N.ctypes.byref(dv.struct), N.ctypes.byref(dh.layers[0].struct),
            N.ptr(dh.top_rows), dh.ntop, N.P(Q.ctypes.data), m, N.ctypes.byref(params), dh.d_nn1_max,
-           N.ptr(st.q_f32), N.ptr(st.chunk_flags), N.ptr(st.epoch_pin), nchunks, narrow, N.ptr(st.ids),
-           N.ptr(st.dists), N.ptr(st.cnt), N.ptr(st.status), N.ptr(ids_h), N.ptr(dists_h), N.ptr(cnt_h),
-           N.ptr(st.status_pin), N.P(search_s.cuda_stream), N.P(copy_s.cuda_stream))
+           q_f32, flags, epoch_pin, nchunks, narrow, ids_d, dists_d, cnt_d, status_d, N.ptr(ids_h),
+           N.ptr(dists_h), N.ptr(cnt_h), status_pin, N.P(search_s.cuda_stream), N.P(copy_s.cuda_stream))
+    st.prepare_spare(m, k)
     for s_ in streams:
         main.wait_stream(s_)
     search_s.synchronize()
     copy_s.synchronize()
-    if int(st.status_pin[0]) != 0:
+    if int(st.status_np[0]) != 0:
         return None
     return BatchResult(ids_h.numpy(), dists_h.numpy(), cnt_h.numpy())
 
