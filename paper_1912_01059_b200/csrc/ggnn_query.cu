@@ -89,6 +89,11 @@ constexpr int SEARCH_MIN_BLOCKS = GGNN_SEARCH_MIN_BLOCKS;
 #ifndef GGNN_U8_MIN_BLOCKS
 #define GGNN_U8_MIN_BLOCKS GGNN_SEARCH_MIN_BLOCKS
 #endif
+// resident CTAs per SM the intermediate resume round of a uint8 batch is
+// compiled for (0: the default)
+#ifndef GGNN_ROUND1_MIN_BLOCKS
+#define GGNN_ROUND1_MIN_BLOCKS 32
+#endif
 template <typename TX, typename TQ>
 constexpr int min_blocks() {
   return (sizeof(TX) == 1 && sizeof(TQ) == 1) ? GGNN_U8_MIN_BLOCKS / GGNN_SEARCH_WARPS : SEARCH_MIN_BLOCKS;
@@ -452,8 +457,13 @@ __global__ void __launch_bounds__(SEARCH_THREADS, (STAGED && STAGED_CAP && sizeo
 // Resume pass of the longest-first schedule: warp w continues parked search
 // park_order[w] to its end, or (pilot > 0: an intermediate round) up to
 // `pilot` expansions in total and parks it again with a fresh prediction.
-template <typename TX, typename TQ, int LP>
-__global__ void __launch_bounds__(SEARCH_THREADS, min_blocks<TX, TQ>()) resume_kernel(const __grid_constant__ SearchArgs a) {
+// MB > 0: this many resident CTAs per SM for the register budget (the
+// intermediate round is throughput-bound: every search runs a bounded number
+// of expansions, so more co-resident searches pay; the last round is bound by
+// its longest searches and keeps the default)
+template <typename TX, typename TQ, int LP, int MB = 0>
+__global__ void __launch_bounds__(SEARCH_THREADS, MB > 0 ? MB : min_blocks<TX, TQ>())
+    resume_kernel(const __grid_constant__ SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   int vring_lane[VR_SLOTS > 0 ? VR_SLOTS : 1];
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1161,7 +1171,8 @@ int launch_query(SearchArgs a, cudaStream_t st) {
   b.park_count = count;
   if (rc == GGNN_OK && P2 > P && a.c.max_steps > P2) {
     b.pilot = P2;
-    rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS);
+    constexpr int MB1 = (sizeof(TX) == 1 && sizeof(TQ) == 1) ? GGNN_ROUND1_MIN_BLOCKS : 0;
+    rc = launch_static(resume_kernel<TX, TQ, LP, MB1>, b, a.m, a.region, st, SEARCH_WARPS);
     if (rc == GGNN_OK) {
       park_order_kernel<<<1, PARK_BUCKETS, 0, st>>>(a.park_key, a.m, order, count);
       count_launch();
