@@ -138,6 +138,13 @@ int ggnn_query_batch(const ggnn_vectors *X, const ggnn_layer *bottom, const int3
  * Process-wide. */
 int ggnn_query_schedule(long long pilot_steps, double min_waves);
 
+/* Large batches (no reference counterpart -- results never depend on it):
+ * uint8 batches of at least large_waves waves of resident searches (default
+ * 3.5) are throughput-bound, so their second round runs up to
+ * GGNN_PILOT2_LARGE = 40 expansions and their last round uses a kernel
+ * compiled for 32 CTAs per SM.  large_waves <= 0 disables.  Process-wide. */
+int ggnn_query_schedule_large(double large_waves);
+
 /* Number of kernels this library has launched in this process (all entry
  * points; no reference counterpart): the bench reads it around its timed
  * region to report gpu_launches. */

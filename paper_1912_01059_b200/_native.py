@@ -80,6 +80,7 @@ _SIGS = {
     "ggnn_search_accounting": [P],
     "ggnn_query_schedule": [I64, F64],
     "ggnn_kernel_launches": [],
+    "ggnn_query_schedule_large": [F64],
     "ggnn_merge_descent": [P, P, I32, I32, I32, P, I64, P, I32, I32, P, P, P, P, P],
     "ggnn_merge_rows": [I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],
     "ggnn_merge_rows_range": [I64, I64, I32, I32, P, P, P, P, P, P, I32, P, P, P, P],

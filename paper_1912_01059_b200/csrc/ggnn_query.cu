@@ -1081,6 +1081,11 @@ constexpr size_t PARK_MAX_BYTES = size_t(4) << 30;
 
 long long g_pilot = -1;        // < 0: GGNN_PILOT or the default
 double g_min_waves = 1.5;       // batches of fewer waves launch plainly
+// uint8 batches of at least this many waves (of default residency) are
+// throughput-bound rather than bound by their longest searches: their second
+// round runs to GGNN_PILOT2_LARGE expansions and their last round is compiled
+// for 32 CTAs per SM (ggnn_query_schedule_large; <= 0 disables)
+double g_large_waves = 3.5;
 
 long long pilot_steps() {
   if (g_pilot >= 0) return g_pilot;
@@ -1097,6 +1102,13 @@ long long pilot2_steps() {
   static const long long P = [] {
     const char* e = getenv("GGNN_PILOT2");
     return e ? atoll(e) : 32LL;
+  }();
+  return P;
+}
+long long pilot2_large_steps() {
+  static const long long P = [] {
+    const char* e = getenv("GGNN_PILOT2_LARGE");
+    return e ? atoll(e) : 40LL;
   }();
   return P;
 }
@@ -1143,9 +1155,12 @@ int launch_query(SearchArgs a, cudaStream_t st) {
   const size_t slot = WarpSearch<TX, TQ, LP>::park_bytes(a.c, a.d * (int64_t)sizeof(TQ));
   const size_t bytes = (size_t)a.m * (slot + 8) + 16;
   bool sched = P > 0 && !a.ever && a.m > 0 && bytes <= PARK_MAX_BYTES && a.c.max_steps > P;
+  bool large = false;
   if (sched) {
     const int64_t res = resident_searches(qk, a.region);
     sched = res > 0 && (double)a.m >= g_min_waves * (double)res;
+    large = sched && sizeof(TX) == 1 && sizeof(TQ) == 1 && g_large_waves > 0.0 &&
+            (double)a.m >= g_large_waves * (double)res;
   }
   if (!sched) return launch_warps(qk, a, a.m, a.region, st);
   keep_default_pool();
@@ -1165,7 +1180,7 @@ int launch_query(SearchArgs a, cudaStream_t st) {
     rc = cudaGetLastError() == cudaSuccess ? GGNN_OK : GGNN_E_CUDA;
     if (rc) set_error("park_order_kernel launch failed");
   }
-  const long long P2 = pilot2_steps();
+  const long long P2 = large ? pilot2_large_steps() : pilot2_steps();
   SearchArgs b = a;
   b.park_order = order;
   b.park_count = count;
@@ -1186,7 +1201,9 @@ int launch_query(SearchArgs a, cudaStream_t st) {
       const char* e = getenv("GGNN_OCC_CAP");
       return e ? atoi(e) : 0;
     }();
-    rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS, occ);
+    constexpr int MB1 = (sizeof(TX) == 1 && sizeof(TQ) == 1) ? GGNN_ROUND1_MIN_BLOCKS : 0;
+    if (large) rc = launch_static(resume_kernel<TX, TQ, LP, MB1>, b, a.m, a.region, st, SEARCH_WARPS, occ);
+    else rc = launch_static(resume_kernel<TX, TQ, LP>, b, a.m, a.region, st, SEARCH_WARPS, occ);
   }
   cudaFreeAsync(buf, st);
   return rc;
@@ -1357,6 +1374,11 @@ int ggnn_search_accounting(unsigned long long* d_acc) {
   return GGNN_OK;
 }
 unsigned long long ggnn_kernel_launches(void) { return ggnn::g_kernel_launches.load(); }
+
+int ggnn_query_schedule_large(double large_waves) {
+  g_large_waves = large_waves;
+  return GGNN_OK;
+}
 
 int ggnn_query_schedule(long long pilot_steps, double min_waves) {
   GGNN_CHECK_ARG(min_waves >= 0.0, "min_waves must be >= 0");

@@ -499,6 +499,27 @@ def test_longest_first_schedule_bitwise(golden_sift, schedule):
     np.testing.assert_array_equal(_arrays(h, Q, cases[0])[0][: len(queries)], g["q6_ids"])
 
 
+def test_large_batch_schedule_bitwise(golden_sift, schedule):
+    """The large-batch variant (second round to 40 expansions, last round on
+    the 32-CTA kernel) returns exactly the plain launch's answers."""
+    g, h, queries = golden_sift
+    reps = -(-2100 // len(queries))
+    Q = np.ascontiguousarray(np.tile(queries, (reps, 1))[:2100]).astype(np.float32)
+    cfg = ga.QueryConfig(k_out=10, tau=0.6)
+    try:
+        for host in (True, False):
+            schedule(0)
+            want = _arrays(h, Q, cfg, host)
+            schedule(8)
+            N.call("ggnn_query_schedule_large", 1e-9)
+            got = _arrays(h, Q, cfg, host)
+            N.call("ggnn_query_schedule_large", 3.5)
+            for w, x in zip(want, got):
+                np.testing.assert_array_equal(w, x)
+    finally:
+        N.call("ggnn_query_schedule_large", 3.5)
+
+
 def test_longest_first_schedule_float_and_mixed(schedule):
     """The same on a float table (FP64 keys, exact re-score) and on a uint8
     table searched with fractional float queries (mixed key path)."""

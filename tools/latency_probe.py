@@ -34,6 +34,8 @@ from paper_1912_01059_b200 import search as S  # noqa: E402
 qflags = 0 if os.environ.get("GGNN_NO_UNIQUE") else S._qflags(dh, False)
 print("flags", qflags)
 params = N.search_params(10, 256, 512, tau, 1000, qflags)
+if os.environ.get("LARGE_WAVES"):  # large-batch variant threshold (ggnn_query_schedule_large)
+    N.call("ggnn_query_schedule_large", float(os.environ["LARGE_WAVES"]))
 Qall = np.concatenate([Q, Q[::-1]])
 sizes = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [148, 592, 1184, 2368, 4144, 6000, 8000,
                                                                            10000, 20000]
