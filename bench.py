@@ -701,7 +701,9 @@ def run_index(args, dist, torch):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch, "kernel_ms": avg_launch * 1e3,
-                     "kernel": f"query_kernel ({'uint8' if dv.exact_integers else 'float32'} table)",
+                     "kernel": f"one ggnn_query_batch launch ({'uint8' if dv.exact_integers else 'float32'} table): "
+                               "pilot query_kernel + park_order_kernel + resume_kernel rounds when the batch "
+                               "is >= 1.5 waves (longest-first schedule), one query_kernel otherwise",
                      "peak_source": peak_src},
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
